@@ -1,0 +1,157 @@
+/*
+ * spconv_b200.h -- C ABI of the B200-native sparse direct-convolution path.
+ *
+ * Drop-in replacement for the hot path of the reference `spconv` library
+ * (SparseTrain, arXiv 1911.10175): the three training passes FWD / BWI / BWW
+ * over dense blocked fp32 tensors that skip work on zeros ReLU puts into the
+ * checked tensor.  Every entry point below replaces one reference interface
+ * (cited as P/<file>:<line>, P = /root/reference/proj):
+ *
+ *   spc_sparse_fwd      <- spconv::sparse_fwd    P/include/spconv/kernels.hpp:58-61
+ *   spc_sparse_bwi      <- spconv::sparse_bwi    P/include/spconv/kernels.hpp:65-69
+ *   spc_sparse_bww      <- spconv::sparse_bww    P/include/spconv/kernels.hpp:74-78
+ *   spc_run_parallel    <- spconv::run_parallel  P/include/spconv/kernels.hpp:83-86
+ *   spc_plan_make       <- spconv::plan          P/include/spconv/planner.hpp:44-46
+ *   spc_shape_make      <- conv_shape::make      P/include/spconv/tensor.hpp:39-40
+ *   spc_shape_validate  <- conv_shape::validate  P/include/spconv/tensor.hpp:47
+ *   spc_native_backend_available <- native_backend_available  kernels.hpp:53
+ *   spc_backend_name    <- conv_result::backend / backend_names  kernels.hpp:47-54
+ *   spc_relu / spc_relu_grad_mask <- relu / relu_grad_mask  P/include/spconv/sparsity.hpp:14-18
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ types or exceptions cross the ABI.
+ *   - `spc_sparse_*` take DEVICE pointers and enqueue on `stream`
+ *     (a cudaStream_t, NULL = legacy default stream); they never synchronize.
+ *   - `spc_sparse_*_host` take HOST pointers: H2D, kernels, D2H, synchronize.
+ *     They are the exact-semantics drop-in (the reference is synchronous).
+ *   - Every contract violation the reference turns into `throw spconv::error`
+ *     (P/src/kernels.cpp:104-142, P/src/tensor.cpp:26-36, P/src/planner.cpp:33-64)
+ *     returns a nonzero spc_status BEFORE any device work, with the message in
+ *     spc_last_error() (thread-local).
+ *   - Outputs are zero-initialised then written (P/src/kernels.cpp:183);
+ *     results are bitwise deterministic run to run (no float atomics).
+ */
+#ifndef SPCONV_B200_H
+#define SPCONV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPC_ABI_VERSION 1
+
+typedef enum {
+    SPC_OK = 0,
+    SPC_ERR_SHAPE = 1,     /* conv_shape::validate failure        (P/src/tensor.cpp:26-36) */
+    SPC_ERR_PLAN = 2,      /* plan/component/Q/ring checks        (P/src/kernels.cpp:104-117, planner.cpp:33-64) */
+    SPC_ERR_LAYOUT = 3,    /* layout / V / dims / size mismatch   (P/src/kernels.cpp:119-142) */
+    SPC_ERR_ARG = 4,       /* null pointer, bad enum, small buffer */
+    SPC_ERR_CUDA = 5,      /* CUDA runtime / launch failure */
+    SPC_ERR_NCCL = 6,      /* collective failure */
+    SPC_ERR_NO_DEVICE = 7  /* no sm_100 device visible */
+} spc_status;
+
+/* conv_shape, field for field (P/include/spconv/tensor.hpp:30-38). */
+typedef struct {
+    int N, C, K, H, W, R, S, O, P, padW, padH;
+} spc_shape;
+
+typedef enum { SPC_FWD = 0, SPC_BWI = 1, SPC_BWW = 2 } spc_component;         /* planner.hpp:18 */
+typedef enum { SPC_CHECK_INPUT = 0, SPC_CHECK_OUTPUT_GRAD = 1 } spc_bww_check; /* planner.hpp:19 */
+typedef enum { SPC_SPARSE = 0, SPC_DENSE = 1 } spc_run_mode;                   /* kernels.hpp:24 */
+
+/* kernel_plan, field for field (P/include/spconv/planner.hpp:22-38).
+ * On the GPU, Q/ring/M do not shape the tiling; they are validated like
+ * check_common and Q keeps its counter semantics. */
+typedef struct {
+    int comp, check, V, Q, T, pipelined, ring_size, M, register_budget, unroll_hint, prefetch_hints;
+} spc_plan;
+
+/* kernel_counters (P/include/spconv/kernels.hpp:31-45).
+ * executed_vector_fmas is counted in-kernel (exact, integer);
+ * checked_vectors and output_vector_loads/stores are the reference's
+ * as-if values (data-independent, computed from shape + plan). */
+typedef struct {
+    uint64_t checked_vectors;
+    uint64_t executed_vector_fmas;
+    uint64_t output_vector_loads;
+    uint64_t output_vector_stores;
+} spc_counters;
+
+/* tensor_layout (P/include/spconv/tensor.hpp:76). */
+typedef enum {
+    SPC_LAYOUT_PLAIN = 0,
+    SPC_LAYOUT_ACT_NCHWC = 1,       /* [N][C/V][H][W][V]            */
+    SPC_LAYOUT_FILTER_KCRS_BLK = 2, /* [K/V][C/V][S][R][Vc][Vk]     */
+    SPC_LAYOUT_ACT_CHWNN = 3        /* [ceil(N/V)][C][H][W][V]      */
+} spc_layout;
+
+/* blocked_tensor header + data pointer (P/include/spconv/tensor.hpp:80-96).
+ * Activation layouts use n/c/h/w; the filter layout uses k/c/s/r.
+ * `numel` is the element count of `data` (for outputs: its capacity). */
+typedef struct {
+    int layout, V;
+    int n, c, h, w;
+    int k, r, s;
+    float* data;
+    size_t numel;
+} spc_tensor;
+
+/* ---- geometry and planning (host only, no device needed) ---- */
+spc_status spc_shape_make(int N, int C, int K, int H, int W, int R, int S, int O, int P, spc_shape* out);
+spc_status spc_shape_make_padded(int N, int C, int K, int H, int W, int R, int S, int O, int P, int padW,
+                                 int padH, spc_shape* out);
+spc_status spc_shape_validate(const spc_shape* shape);
+spc_status spc_plan_make(const spc_shape* shape, int comp, int V, int register_budget, int check, spc_plan* out);
+/* Header (layout, dims, numel) of the output a pass produces; data = NULL. */
+spc_status spc_output_desc(const spc_shape* shape, const spc_plan* plan, spc_tensor* out);
+/* The as-if counters (checked, loads, stores) for a pass; executed = dense total
+ * in dense mode, 0 in sparse mode (the kernels add the executed count). */
+spc_status spc_analytic_counters(const spc_shape* shape, const spc_plan* plan, int mode, spc_counters* out);
+
+/* ---- the three passes on device buffers (asynchronous on `stream`) ---- */
+/* FWD: src = D (ActNCHWc over C), filt = G (FilterKCRSblk K,C); dst = Y (ActNCHWc over K). */
+spc_status spc_sparse_fwd(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
+                          const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
+                          void* stream);
+/* BWI: src = dY (ActNCHWc over K), filt = G^T (pack_filter swap_kc: FilterKCRSblk C,K);
+ * dst = dD (ActNCHWc over C). */
+spc_status spc_sparse_bwi(const spc_tensor* grad_out, const spc_tensor* filt_t, const spc_shape* shape,
+                          const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
+                          void* stream);
+/* BWW: the tensor named by plan->check is ActCHWNn, the other ActNCHWc;
+ * dst = dG (FilterKCRSblk K,C) for either check side. */
+spc_status spc_sparse_bww(const spc_tensor* input, const spc_tensor* grad_out, const spc_shape* shape,
+                          const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
+                          void* stream);
+/* Dispatch on plan->comp (a = swept tensor or input, b = filters or grad_out). */
+spc_status spc_run_parallel(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
+                            const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
+                            void* stream);
+
+/* ---- host-buffer drop-ins: copy in, run, copy out, synchronize ---- */
+spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
+                                 const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters);
+
+/* ---- ReLU semantics on device (P/src/sparsity.cpp:11-28), bit-exact ---- */
+spc_status spc_relu(const float* in, float* out, size_t n, void* stream);
+spc_status spc_relu_grad_mask(const float* pre, const float* upstream, float* out, size_t n, void* stream);
+
+/* ---- device layout conversion: ActNCHWc -> ActCHWNn (tensor.cpp:94-108) ---- */
+spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stream);
+
+/* ---- introspection ---- */
+const char* spc_last_error(void);
+const char* spc_backend_name(void);
+int spc_native_backend_available(int V);
+int spc_abi_version(void);
+/* Count of device kernels this library has launched in this process. */
+uint64_t spc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCONV_B200_H */

@@ -1,0 +1,613 @@
+// capi.cu -- the extern "C" boundary: validation, planning, counters, dispatch.
+//
+// Validation restates the reference's contract checks so that the same bad
+// calls fail the same way, before any device work:
+//   conv_shape::validate      P/src/tensor.cpp:26-36
+//   plan()                    P/src/planner.cpp:25-73
+//   check_common              P/src/kernels.cpp:104-117
+//   check_act / check_filter  P/src/kernels.cpp:119-142
+//   per-entry C,K % V checks  P/src/kernels.cpp:172-173, 208-209, 244-245
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dispatch.h"
+
+namespace spc {
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static thread_local std::string g_err;
+
+static spc_status fail(spc_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+static bool valid_V(int v) { return v == 4 || v == 8 || v == 16; }
+static int out_w(const spc_shape& s) { return (s.W + 2 * s.padW - s.R) / s.O + 1; }
+static int out_h(const spc_shape& s) { return (s.H + 2 * s.padH - s.S) / s.P + 1; }
+
+// conv_shape::validate (P/src/tensor.cpp:26-36)
+static spc_status validate_shape(const spc_shape& s) {
+    if (!(s.N > 0 && s.C > 0 && s.K > 0 && s.H > 0 && s.W > 0 && s.R > 0 && s.S > 0))
+        return fail(SPC_ERR_SHAPE, "conv_shape: all dimensions must be positive");
+    if (!(s.O >= 1 && s.P >= 1)) return fail(SPC_ERR_SHAPE, "conv_shape: strides must be >= 1");
+    if (!(s.padW >= 0 && s.padH >= 0 && s.padW < s.R && s.padH < s.S))
+        return fail(SPC_ERR_SHAPE, "conv_shape: padding must satisfy 0 <= pad < filter size");
+    if (!(s.W + 2 * s.padW >= s.R && s.H + 2 * s.padH >= s.S))
+        return fail(SPC_ERR_SHAPE, "conv_shape: filter does not fit the padded image");
+    if (!(out_w(s) >= 1 && out_h(s) >= 1)) return fail(SPC_ERR_SHAPE, "conv_shape: output size must be positive");
+    return SPC_OK;
+}
+
+// kernel_plan::tiled_channels (P/src/planner.cpp:18-23)
+static int tiled_channels(const spc_shape& s, int comp, int check) {
+    if (comp == SPC_BWI) return s.C;
+    if (comp == SPC_BWW && check == SPC_CHECK_OUTPUT_GRAD) return s.C;
+    return s.K;
+}
+
+// check_common (P/src/kernels.cpp:104-117); max_ring_vectors = 64 (kernel_impl.hpp:19)
+static spc_status check_common(const spc_shape& sh, const spc_plan& pl, int comp) {
+    spc_status st = validate_shape(sh);
+    if (st) return st;
+    if (pl.comp != comp) return fail(SPC_ERR_PLAN, "plan was built for another component");
+    if (!valid_V(pl.V)) return fail(SPC_ERR_PLAN, "plan has an invalid V");
+    if (comp == SPC_BWW && pl.check != SPC_CHECK_INPUT && pl.check != SPC_CHECK_OUTPUT_GRAD)
+        return fail(SPC_ERR_PLAN, "plan has an invalid bww check side");
+    const int tiled = tiled_channels(sh, comp, pl.check);
+    if (!(pl.Q >= pl.V && pl.Q % pl.V == 0 && tiled % pl.Q == 0))
+        return fail(SPC_ERR_PLAN, "plan tile Q does not divide the tiled channel dim");
+    const int ring_need = (sh.R + (pl.pipelined ? 1 : 0)) * pl.Q / pl.V;
+    if (ring_need > 64) return fail(SPC_ERR_PLAN, "plan ring size exceeds the kernel accumulator bound");
+    return SPC_OK;
+}
+
+// check_act (P/src/kernels.cpp:119-132)
+static spc_status check_act(const spc_tensor* t, int want, int V, int n, int ch, int rows, int cols,
+                            const char* what) {
+    if (!t) return fail(SPC_ERR_ARG, std::string(what) + ": null tensor");
+    if (t->layout != want) return fail(SPC_ERR_LAYOUT, std::string(what) + ": wrong layout");
+    if (t->V != V) return fail(SPC_ERR_LAYOUT, std::string(what) + ": wrong vector width");
+    if (!(t->n == n && t->c == ch && t->h == rows && t->w == cols))
+        return fail(SPC_ERR_LAYOUT, std::string(what) + ": dims do not match shape");
+    const size_t expect = want == SPC_LAYOUT_ACT_CHWNN ? (size_t)((n + V - 1) / V) * ch * rows * cols * V
+                                                       : (size_t)n * ch * rows * cols;
+    if (t->numel != expect) return fail(SPC_ERR_LAYOUT, std::string(what) + ": data size mismatch");
+    if (!t->data) return fail(SPC_ERR_ARG, std::string(what) + ": null data");
+    return SPC_OK;
+}
+
+// check_filter (P/src/kernels.cpp:134-142)
+static spc_status check_filter(const spc_tensor* t, int V, int k, int c, int s, int r, const char* what) {
+    if (!t) return fail(SPC_ERR_ARG, std::string(what) + ": null tensor");
+    if (t->layout != SPC_LAYOUT_FILTER_KCRS_BLK) return fail(SPC_ERR_LAYOUT, std::string(what) + ": wrong layout");
+    if (t->V != V) return fail(SPC_ERR_LAYOUT, std::string(what) + ": wrong vector width");
+    if (!(t->k == k && t->c == c && t->s == s && t->r == r))
+        return fail(SPC_ERR_LAYOUT, std::string(what) + ": dims do not match shape");
+    if (t->numel != (size_t)k * c * s * r) return fail(SPC_ERR_LAYOUT, std::string(what) + ": data size mismatch");
+    if (!t->data) return fail(SPC_ERR_ARG, std::string(what) + ": null data");
+    return SPC_OK;
+}
+
+static void set_act_desc(spc_tensor* t, int V, int n, int c, int h, int w) {
+    t->layout = SPC_LAYOUT_ACT_NCHWC;
+    t->V = V;
+    t->n = n; t->c = c; t->h = h; t->w = w;
+    t->k = t->r = t->s = 0;
+}
+
+static void set_filter_desc(spc_tensor* t, int V, int k, int c, int s, int r) {
+    t->layout = SPC_LAYOUT_FILTER_KCRS_BLK;
+    t->V = V;
+    t->k = k; t->c = c; t->s = s; t->r = r;
+    t->n = t->h = t->w = 0;
+}
+
+static spc_status output_desc(const spc_shape& sh, const spc_plan& pl, spc_tensor* out) {
+    const size_t cap = out->numel;
+    float* data = out->data;
+    if (pl.comp == SPC_FWD) {
+        set_act_desc(out, pl.V, sh.N, sh.K, out_h(sh), out_w(sh));
+        out->numel = (size_t)sh.N * sh.K * out_h(sh) * out_w(sh);
+    } else if (pl.comp == SPC_BWI) {
+        set_act_desc(out, pl.V, sh.N, sh.C, sh.H, sh.W);
+        out->numel = (size_t)sh.N * sh.C * sh.H * sh.W;
+    } else {
+        set_filter_desc(out, pl.V, sh.K, sh.C, sh.S, sh.R);
+        out->numel = (size_t)sh.K * sh.C * sh.S * sh.R;
+    }
+    (void)cap;
+    out->data = data;
+    return SPC_OK;
+}
+
+// Output tensor: header is written by the call; the caller supplies data with
+// capacity >= the required element count.
+static spc_status prepare_dst(const spc_shape& sh, const spc_plan& pl, spc_tensor* dst) {
+    if (!dst) return fail(SPC_ERR_ARG, "null output tensor");
+    const size_t cap = dst->numel;
+    float* data = dst->data;
+    output_desc(sh, pl, dst);
+    if (!data) return fail(SPC_ERR_ARG, "null output data");
+    if (cap < dst->numel) return fail(SPC_ERR_ARG, "output buffer too small");
+    return SPC_OK;
+}
+
+// ---------------------------------------------------------------- counters
+// As-if counters of the reference kernels (P/src/kernel_impl.hpp:129-198,
+// 229-325).  checked_vectors and the ring loads/stores depend only on shape
+// and plan; dense-mode executed FMAs equal the dense total.
+static void analytic_counters(const spc_shape& sh, const spc_plan& pl, int mode, spc_counters* c) {
+    std::memset(c, 0, sizeof(*c));
+    const int V = pl.V, hp = out_h(sh), wp = out_w(sh);
+    const unsigned long long qv = (unsigned long long)(pl.Q / V);
+    if (pl.comp == SPC_FWD || pl.comp == SPC_BWI) {
+        const bool fwd = pl.comp == SPC_FWD;
+        unsigned long long rows = 0;  // valid (output row, filter row) pairs
+        const int orows = fwd ? hp : sh.H;
+        for (int orow = 0; orow < orows; ++orow)
+            for (int v = 0; v < sh.S; ++v) {
+                if (fwd) {
+                    const int y = orow * sh.P + v - sh.padH;
+                    if (y < 0 || y >= sh.H) continue;
+                } else {
+                    const int num = orow + sh.padH - v;
+                    if (num < 0 || num % sh.P != 0 || num / sh.P >= hp) continue;
+                }
+                ++rows;
+            }
+        const int scols = fwd ? sh.W : wp;  // swept columns
+        const int ocols = fwd ? wp : sh.W;
+        std::vector<char> touched(ocols, 0);
+        unsigned long long tsum = 0;
+        for (int x = 0; x < scols; ++x) {
+            for (int u = 0; u < sh.R; ++u) {
+                int oc;
+                if (fwd) {
+                    const int num = x + sh.padW - u;
+                    if (num < 0 || num % sh.O != 0) continue;
+                    oc = num / sh.O;
+                    if (oc >= wp) continue;
+                } else {
+                    oc = x * sh.O + u - sh.padW;
+                    if (oc < 0 || oc >= sh.W) continue;
+                }
+                touched[oc] = 1;
+                ++tsum;
+            }
+        }
+        unsigned long long ntouched = 0;
+        for (char t : touched) ntouched += t;
+        const int red_blocks = (fwd ? sh.C : sh.K) / V;
+        const unsigned long long tiles = (unsigned long long)(fwd ? sh.K : sh.C) / pl.Q;
+        const unsigned long long sweeps = rows * red_blocks * (unsigned long long)sh.N * tiles;
+        c->output_vector_loads = c->output_vector_stores = sweeps * ntouched * qv;
+        if (mode == SPC_SPARSE) {
+            c->checked_vectors = tiles * rows * sh.N * (unsigned long long)red_blocks * scols;
+        } else {
+            c->executed_vector_fmas = rows * sh.N * (unsigned long long)red_blocks * V * tsum * qv * tiles;
+        }
+    } else {
+        const bool on_input = pl.check == SPC_CHECK_INPUT;
+        unsigned long long rows = 0;
+        for (int v = 0; v < sh.S; ++v)
+            for (int yp = 0; yp < hp; ++yp) {
+                const int y = yp * sh.P + v - sh.padH;
+                if (y >= 0 && y < sh.H) ++rows;
+            }
+        const int chans = on_input ? sh.C : sh.K;
+        const int cols = on_input ? sh.W : wp;
+        const unsigned long long tiles = (unsigned long long)(on_input ? sh.K : sh.C) / pl.Q;
+        const unsigned long long nb = (unsigned long long)((sh.N + V - 1) / V);
+        unsigned long long tsum = 0;
+        for (int x = 0; x < cols; ++x)
+            for (int u = 0; u < sh.R; ++u) {
+                if (on_input) {
+                    const int num = x + sh.padW - u;
+                    if (num < 0 || num % sh.O != 0 || num / sh.O >= wp) continue;
+                } else {
+                    const int xx = x * sh.O + u - sh.padW;
+                    if (xx < 0 || xx >= sh.W) continue;
+                }
+                ++tsum;
+            }
+        c->output_vector_loads = c->output_vector_stores = rows * nb * chans * tiles * sh.R * qv;
+        if (mode == SPC_SPARSE) {
+            c->checked_vectors = tiles * rows * chans * nb * cols;
+        } else {
+            c->executed_vector_fmas = rows * chans * (unsigned long long)sh.N * tsum * qv * tiles;
+        }
+    }
+}
+
+__global__ void counters_init_kernel(spc_counters* c, spc_counters v) { *c = v; }
+
+// ---------------------------------------------------------------- device
+static spc_status check_device() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SPC_ERR_NO_DEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    static int cached_ok[64] = {0};
+    if (dev >= 0 && dev < 64 && cached_ok[dev] == 1) return SPC_OK;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(SPC_ERR_NO_DEVICE, "this library is built for sm_100a (B200); device is sm_" +
+                                           std::to_string(major) + std::to_string(minor));
+    // keep stream-ordered workspace allocations cached between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (dev >= 0 && dev < 64) cached_ok[dev] = 1;
+    return SPC_OK;
+}
+
+static spc_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(SPC_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static spc_status start_counters(const spc_shape& sh, const spc_plan& pl, int mode, spc_counters* d_counters,
+                                 cudaStream_t st) {
+    if (!d_counters) return SPC_OK;
+    spc_counters init;
+    analytic_counters(sh, pl, mode, &init);
+    counters_init_kernel<<<1, 1, 0, st>>>(d_counters, init);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "counters init");
+}
+
+static unsigned long long* exec_slot(spc_counters* d_counters, int mode) {
+    // dense mode reports the analytic dense total; only sparse mode counts
+    if (!d_counters || mode != SPC_SPARSE) return nullptr;
+    return reinterpret_cast<unsigned long long*>(&d_counters->executed_vector_fmas);
+}
+
+// ---------------------------------------------------------------- passes
+static spc_status validate_fwd(const spc_tensor* src, const spc_tensor* filt, const spc_shape& sh,
+                               const spc_plan& pl) {
+    spc_status st = check_common(sh, pl, SPC_FWD);
+    if (st) return st;
+    const int V = pl.V;
+    if (sh.C % V || sh.K % V) return fail(SPC_ERR_SHAPE, "fwd: C and K must be multiples of V");
+    if ((st = check_act(src, SPC_LAYOUT_ACT_NCHWC, V, sh.N, sh.C, sh.H, sh.W, "fwd input"))) return st;
+    return check_filter(filt, V, sh.K, sh.C, sh.S, sh.R, "fwd filter");
+}
+
+static spc_status validate_bwi(const spc_tensor* dy, const spc_tensor* filt_t, const spc_shape& sh,
+                               const spc_plan& pl) {
+    spc_status st = check_common(sh, pl, SPC_BWI);
+    if (st) return st;
+    const int V = pl.V;
+    if (sh.C % V || sh.K % V) return fail(SPC_ERR_SHAPE, "bwi: C and K must be multiples of V");
+    if ((st = check_act(dy, SPC_LAYOUT_ACT_NCHWC, V, sh.N, sh.K, out_h(sh), out_w(sh), "bwi gradient")))
+        return st;
+    return check_filter(filt_t, V, sh.C, sh.K, sh.S, sh.R, "bwi transposed filter");
+}
+
+static spc_status validate_bww(const spc_tensor* in, const spc_tensor* dy, const spc_shape& sh,
+                               const spc_plan& pl) {
+    spc_status st = check_common(sh, pl, SPC_BWW);
+    if (st) return st;
+    const int V = pl.V;
+    if (sh.C % V || sh.K % V) return fail(SPC_ERR_SHAPE, "bww: C and K must be multiples of V");
+    if (pl.check == SPC_CHECK_INPUT) {
+        if ((st = check_act(in, SPC_LAYOUT_ACT_CHWNN, V, sh.N, sh.C, sh.H, sh.W, "bww input"))) return st;
+        return check_act(dy, SPC_LAYOUT_ACT_NCHWC, V, sh.N, sh.K, out_h(sh), out_w(sh), "bww gradient");
+    }
+    if ((st = check_act(dy, SPC_LAYOUT_ACT_CHWNN, V, sh.N, sh.K, out_h(sh), out_w(sh), "bww gradient")))
+        return st;
+    return check_act(in, SPC_LAYOUT_ACT_NCHWC, V, sh.N, sh.C, sh.H, sh.W, "bww input");
+}
+
+static spc_status run_fwd_bwi(bool fwd, const spc_tensor* src, const spc_tensor* filt, const spc_shape& sh,
+                              const spc_plan& pl, int mode, spc_tensor* dst, spc_counters* d_counters,
+                              cudaStream_t st) {
+    spc_status s = fwd ? validate_fwd(src, filt, sh, pl) : validate_bwi(src, filt, sh, pl);
+    if (s) return s;
+    if (mode != SPC_SPARSE && mode != SPC_DENSE) return fail(SPC_ERR_ARG, "bad run mode");
+    if ((s = prepare_dst(sh, pl, dst))) return s;
+    if ((s = check_device())) return s;
+    if ((s = start_counters(sh, pl, mode, d_counters, st))) return s;
+    const DevShape ds = make_dev_shape(sh);
+    cudaError_t e = launch_conv(fwd, mode == SPC_SPARSE, ds, pl.V, src->data, filt->data, dst->data,
+                                exec_slot(d_counters, mode), st);
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, fwd ? "fwd launch" : "bwi launch");
+}
+
+static spc_status run_bww(const spc_tensor* in, const spc_tensor* dy, const spc_shape& sh, const spc_plan& pl,
+                          int mode, spc_tensor* dst, spc_counters* d_counters, cudaStream_t st) {
+    spc_status s = validate_bww(in, dy, sh, pl);
+    if (s) return s;
+    if (mode != SPC_SPARSE && mode != SPC_DENSE) return fail(SPC_ERR_ARG, "bad run mode");
+    if ((s = prepare_dst(sh, pl, dst))) return s;
+    if ((s = check_device())) return s;
+    if ((s = start_counters(sh, pl, mode, d_counters, st))) return s;
+    const DevShape ds = make_dev_shape(sh);
+    const bool on_input = pl.check == SPC_CHECK_INPUT;
+    cudaError_t e = launch_bww(on_input, mode == SPC_SPARSE, ds, pl.V, on_input ? in->data : dy->data,
+                               on_input ? dy->data : in->data, dst->data, exec_slot(d_counters, mode), st);
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "bww launch");
+}
+
+// ---------------------------------------------------------------- aux kernels
+__global__ void relu_kernel(const float* __restrict__ in, float* __restrict__ out, size_t n) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const float x = in[e];
+        out[e] = x > 0.0f ? x : 0.0f;  // P/src/sparsity.cpp:13 (-0 and NaN -> +0)
+    }
+}
+
+__global__ void relu_grad_mask_kernel(const float* __restrict__ pre, const float* __restrict__ up,
+                                      float* __restrict__ out, size_t n) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+        out[e] = pre[e] > 0.0f ? up[e] : 0.0f;  // P/src/sparsity.cpp:26: zero where !(pre > 0)
+}
+
+// ActNCHWc -> ActCHWNn with zero-filled ragged tail lanes (P/src/tensor.cpp:94-108).
+__global__ void nchwc_to_chwnn_kernel(const float* __restrict__ src, float* __restrict__ dst, int n, int c,
+                                      int h, int w, int V) {
+    const size_t total = (size_t)((n + V - 1) / V) * c * h * w * V;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)gridDim.x * blockDim.x) {
+        size_t t = e;
+        const int lane = (int)(t % V);
+        t /= V;
+        const int x = (int)(t % w);
+        t /= w;
+        const int y = (int)(t % h);
+        t /= h;
+        const int ch = (int)(t % c);
+        const int ib = (int)(t / c);
+        const int i = ib * V + lane;
+        dst[e] = i < n ? src[act_index(c, h, w, V, i, ch, y, x)] : 0.0f;
+    }
+}
+
+static unsigned grid_for(size_t n) {
+    size_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    if (b == 0) b = 1;
+    return (unsigned)b;
+}
+
+}  // namespace spc
+
+using namespace spc;
+
+// ================================================================ C ABI
+extern "C" {
+
+int spc_abi_version(void) { return SPC_ABI_VERSION; }
+const char* spc_last_error(void) { return g_err.c_str(); }
+const char* spc_backend_name(void) { return "cuda-sm100a"; }
+uint64_t spc_launch_count(void) { return g_launches.load(); }
+
+int spc_native_backend_available(int V) {
+    if (!valid_V(V)) return 0;
+    return check_device() == SPC_OK ? 1 : 0;
+}
+
+spc_status spc_shape_make_padded(int N, int C, int K, int H, int W, int R, int S, int O, int P, int padW,
+                                 int padH, spc_shape* out) {
+    if (!out) return fail(SPC_ERR_ARG, "null shape");
+    spc_shape s = {N, C, K, H, W, R, S, O, P, padW, padH};
+    *out = s;
+    return validate_shape(s);
+}
+
+spc_status spc_shape_make(int N, int C, int K, int H, int W, int R, int S, int O, int P, spc_shape* out) {
+    return spc_shape_make_padded(N, C, K, H, W, R, S, O, P, (R - 1) / 2, (S - 1) / 2, out);
+}
+
+spc_status spc_shape_validate(const spc_shape* shape) {
+    if (!shape) return fail(SPC_ERR_ARG, "null shape");
+    return validate_shape(*shape);
+}
+
+// plan() (P/src/planner.cpp:25-73): largest ring under the register budget,
+// larger Q on ties, then not pipelining; R=1 tiles capped at 128; bww never
+// pipelines; M = 16 (1 for bww).
+spc_status spc_plan_make(const spc_shape* shape, int comp, int V, int budget, int check, spc_plan* out) {
+    if (!shape || !out) return fail(SPC_ERR_ARG, "null argument");
+    spc_status st = validate_shape(*shape);
+    if (st) return st;
+    if (!valid_V(V)) return fail(SPC_ERR_PLAN, "plan: V must be 4, 8 or 16");
+    if (budget < 1) return fail(SPC_ERR_PLAN, "plan: register budget must be >= 1");
+    if (comp < SPC_FWD || comp > SPC_BWW) return fail(SPC_ERR_ARG, "plan: bad component");
+    spc_plan p;
+    std::memset(&p, 0, sizeof(p));
+    p.comp = comp;
+    p.check = check;
+    p.V = V;
+    p.register_budget = budget;
+    const int ch = tiled_channels(*shape, comp, check);
+    if (ch % V) return fail(SPC_ERR_PLAN, "plan: tiled channel dimension must be a multiple of V");
+    const int R = shape->R;
+    const bool allow_pipe = comp != SPC_BWW;
+    int best_q = 0, best_ring = 0;
+    bool best_pipe = false;
+    for (int q = V; q <= ch; q += V) {
+        if (ch % q) continue;
+        if (R == 1 && q > 128) continue;
+        for (int pipe = 0; pipe <= (allow_pipe ? 1 : 0); ++pipe) {
+            const int ring = (R + pipe) * q / V;
+            if (ring > budget) continue;
+            const bool better =
+                ring > best_ring || (ring == best_ring && (q > best_q || (q == best_q && pipe < (int)best_pipe)));
+            if (better) {
+                best_q = q;
+                best_ring = ring;
+                best_pipe = pipe != 0;
+            }
+        }
+    }
+    if (!best_q) return fail(SPC_ERR_PLAN, "plan: no feasible channel tile fits the register budget");
+    p.Q = best_q;
+    p.T = R * best_q / V;
+    p.pipelined = best_pipe ? 1 : 0;
+    p.ring_size = best_ring;
+    p.M = comp == SPC_BWW ? 1 : 16;
+    p.unroll_hint = best_pipe ? R + 1 : R;
+    *out = p;
+    return SPC_OK;
+}
+
+spc_status spc_output_desc(const spc_shape* shape, const spc_plan* plan, spc_tensor* out) {
+    if (!shape || !plan || !out) return fail(SPC_ERR_ARG, "null argument");
+    spc_status st = validate_shape(*shape);
+    if (st) return st;
+    out->data = nullptr;
+    return output_desc(*shape, *plan, out);
+}
+
+spc_status spc_analytic_counters(const spc_shape* shape, const spc_plan* plan, int mode, spc_counters* out) {
+    if (!shape || !plan || !out) return fail(SPC_ERR_ARG, "null argument");
+    spc_status st = check_common(*shape, *plan, plan->comp);
+    if (st) return st;
+    analytic_counters(*shape, *plan, mode, out);
+    return SPC_OK;
+}
+
+spc_status spc_sparse_fwd(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
+                          const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    return run_fwd_bwi(true, src, filt, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
+}
+
+spc_status spc_sparse_bwi(const spc_tensor* grad_out, const spc_tensor* filt_t, const spc_shape* shape,
+                          const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    return run_fwd_bwi(false, grad_out, filt_t, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
+}
+
+spc_status spc_sparse_bww(const spc_tensor* input, const spc_tensor* grad_out, const spc_shape* shape,
+                          const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    return run_bww(input, grad_out, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
+}
+
+spc_status spc_run_parallel(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape, const spc_plan* plan,
+                            int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    if (!plan) return fail(SPC_ERR_ARG, "null plan");
+    switch (plan->comp) {
+    case SPC_FWD: return spc_sparse_fwd(a, b, shape, plan, mode, dst, d_counters, stream);
+    case SPC_BWI: return spc_sparse_bwi(a, b, shape, plan, mode, dst, d_counters, stream);
+    case SPC_BWW: return spc_sparse_bww(a, b, shape, plan, mode, dst, d_counters, stream);
+    }
+    return fail(SPC_ERR_PLAN, "run_parallel: bad component");
+}
+
+// Host-buffer drop-in: validate, copy in, run, copy out, synchronize.
+spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
+                                 const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters) {
+    if (!a || !b || !shape || !plan || !dst) return fail(SPC_ERR_ARG, "null argument");
+    spc_status st;
+    switch (plan->comp) {
+    case SPC_FWD: st = validate_fwd(a, b, *shape, *plan); break;
+    case SPC_BWI: st = validate_bwi(a, b, *shape, *plan); break;
+    case SPC_BWW: st = validate_bww(a, b, *shape, *plan); break;
+    default: return fail(SPC_ERR_PLAN, "run_parallel: bad component");
+    }
+    if (st) return st;
+    spc_tensor out = *dst;
+    if ((st = prepare_dst(*shape, *plan, &out))) return st;
+    if ((st = check_device())) return st;
+    static thread_local cudaStream_t s_stream = nullptr;
+    static thread_local int s_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!s_stream || s_dev != dev) {
+        cudaError_t e = cudaStreamCreateWithFlags(&s_stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "stream create");
+        s_dev = dev;
+    }
+    cudaStream_t sm = s_stream;
+    float *da = nullptr, *db = nullptr, *dd = nullptr;
+    spc_counters* dc = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync((void**)&da, a->numel * sizeof(float), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if ((e = cudaMallocAsync((void**)&db, b->numel * sizeof(float), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if ((e = cudaMallocAsync((void**)&dd, out.numel * sizeof(float), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if ((e = cudaMallocAsync((void**)&dc, sizeof(spc_counters), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
+    cudaMemcpyAsync(da, a->data, a->numel * sizeof(float), cudaMemcpyHostToDevice, sm);
+    cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, sm);
+    spc_tensor ta = *a, tb = *b, td = out;
+    ta.data = da;
+    tb.data = db;
+    td.data = dd;
+    st = spc_run_parallel(&ta, &tb, shape, plan, mode, &td, counters ? dc : nullptr, sm);
+    if (st == SPC_OK) {
+        cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, sm);
+        if (counters) cudaMemcpyAsync(counters, dc, sizeof(spc_counters), cudaMemcpyDeviceToHost, sm);
+    }
+    cudaFreeAsync(da, sm);
+    cudaFreeAsync(db, sm);
+    cudaFreeAsync(dd, sm);
+    cudaFreeAsync(dc, sm);
+    e = cudaStreamSynchronize(sm);
+    if (st) return st;
+    if (e != cudaSuccess) return cuda_fail(e, "host run");
+    *dst = out;
+    return SPC_OK;
+}
+
+spc_status spc_relu(const float* in, float* out, size_t n, void* stream) {
+    if ((!in || !out) && n) return fail(SPC_ERR_ARG, "null pointer");
+    spc_status st = check_device();
+    if (st) return st;
+    if (!n) return SPC_OK;
+    relu_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(in, out, n);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "relu");
+}
+
+spc_status spc_relu_grad_mask(const float* pre, const float* upstream, float* out, size_t n, void* stream) {
+    if ((!pre || !upstream || !out) && n) return fail(SPC_ERR_ARG, "null pointer");
+    spc_status st = check_device();
+    if (st) return st;
+    if (!n) return SPC_OK;
+    relu_grad_mask_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(pre, upstream, out, n);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "relu_grad_mask");
+}
+
+spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stream) {
+    if (!src || !dst) return fail(SPC_ERR_ARG, "null tensor");
+    if (src->layout != SPC_LAYOUT_ACT_NCHWC) return fail(SPC_ERR_LAYOUT, "nchwc_to_chwnn: source must be ActNCHWc");
+    if (!valid_V(src->V) || src->c % src->V) return fail(SPC_ERR_LAYOUT, "nchwc_to_chwnn: bad V");
+    if (src->numel != (size_t)src->n * src->c * src->h * src->w)
+        return fail(SPC_ERR_LAYOUT, "nchwc_to_chwnn: data size mismatch");
+    const int V = src->V;
+    const size_t need = (size_t)((src->n + V - 1) / V) * src->c * src->h * src->w * V;
+    if (!dst->data || dst->numel < need) return fail(SPC_ERR_ARG, "nchwc_to_chwnn: output buffer too small");
+    spc_status st = check_device();
+    if (st) return st;
+    dst->layout = SPC_LAYOUT_ACT_CHWNN;
+    dst->V = V;
+    dst->n = src->n; dst->c = src->c; dst->h = src->h; dst->w = src->w;
+    dst->k = dst->r = dst->s = 0;
+    dst->numel = need;
+    nchwc_to_chwnn_kernel<<<grid_for(need), 256, 0, (cudaStream_t)stream>>>(src->data, dst->data, src->n, src->c,
+                                                                           src->h, src->w, V);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "nchwc_to_chwnn");
+}
+
+}  // extern "C"

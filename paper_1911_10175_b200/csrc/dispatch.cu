@@ -1,0 +1,23 @@
+// dispatch.cu -- kernel selection (internal).
+#include "dispatch.h"
+
+namespace spc {
+
+cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,
+                        float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    return launch_conv_generic(fwd, sparse, sh, V, src, filt, dst, exec_ctr, st);
+}
+
+cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V, const float* chk,
+                       const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    const int splits = bww_generic_splits(sh);
+    const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
+    float* partial = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)splits * E * sizeof(float), st);
+    if (e != cudaSuccess) return e;
+    e = launch_bww_generic(check_input, sparse, sh, V, chk, oth, partial, splits, dst, exec_ctr, st);
+    cudaFreeAsync(partial, st);
+    return e;
+}
+
+}  // namespace spc

@@ -1,0 +1,340 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Mirrors the reference's hot-path suite P/tests/test_kernels.cpp case for case.
+Bars (BASELINE.json north_star):
+  * fp32 outputs: max|got - ref| / max|ref| <= 1e-5 (TOL below) against the
+    64-bit oracle, and the reference's own elementwise metric <= 1e-4 on the
+    all-positive gen_sparse inputs its tests use;
+  * zero/nonzero indexing: executed_vector_fmas and checked_vectors equal the
+    reference's exact counts (integer equality);
+  * bitwise determinism run to run.
+"""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5  # max-abs-normalised fp32 tolerance (north_star)
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+ALL = [(0, 0), (1, 0), (2, 0), (2, 1)]  # (comp, check)
+
+
+def rng_tiny_shape(rng, V):
+    from test_oracle import rng_tiny_shape as f
+    return f(rng, V)
+
+
+def make_inputs(sp, sh, comp, check, s, V, seed):
+    """testutil::make_inputs (P/tests/testutil.hpp:43-78) with the oracle's
+    bit-identical gen_sparse; returns plain operands + blocked device operands."""
+    t = sh.astuple()
+    N, C, K, H, W, R, S = t[:7]
+    hp, wp = sh.out_h(), sh.out_w()
+    if comp == 0:
+        a, b = O.gen_sparse(N, C, H, W, s, seed), O.gen_sparse(K, C, S, R, 0.0, seed + 1)
+        ba, bb = sp.pack_act_nchwc(a, V), sp.pack_filter(b, V)
+    elif comp == 1:
+        a, b = O.gen_sparse(N, K, hp, wp, s, seed), O.gen_sparse(K, C, S, R, 0.0, seed + 1)
+        ba, bb = sp.pack_act_nchwc(a, V), sp.pack_filter(b, V, True)
+    elif check == 0:
+        a, b = O.gen_sparse(N, C, H, W, s, seed), O.gen_sparse(N, K, hp, wp, 0.0, seed + 2)
+        ba, bb = sp.pack_act_chwnn(a, V), sp.pack_act_nchwc(b, V)
+    else:
+        a, b = O.gen_sparse(N, C, H, W, 0.0, seed), O.gen_sparse(N, K, hp, wp, s, seed + 2)
+        ba, bb = sp.pack_act_nchwc(a, V), sp.pack_act_chwnn(b, V)
+    return a, b, ba.to("cuda"), bb.to("cuda")
+
+
+def run(sp, sh, comp, check, V, ba, bb, mode=0):
+    pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
+    res = sp.run_parallel(ba, bb, sh, pl, sp.RunMode(mode))
+    return pl, res, sp.unpack(res.out).cpu().numpy()
+
+
+def mask_of(comp, check, a, b):
+    return b if (comp == 2 and check == 1) else a
+
+
+def test_kernels_match_oracle_across_sparsities_and_modes(sp):  # test_kernels.cpp:26-47
+    rng = np.random.default_rng(101)
+    for trial in range(24):
+        V = [4, 8, 16][trial % 3]
+        sh = sp.ConvShape(*rng_tiny_shape(rng, V))
+        s = float(rng.choice([0.0, 0.3, 0.5, 0.8, 0.9, 1.0]))
+        for comp, check in ALL:
+            a, b, ba, bb = make_inputs(sp, sh, comp, check, s, V, trial * 7 + 1)
+            ref = O.dense(comp, sh.astuple(), a, b)
+            for mode in (0, 1):
+                _, res, got = run(sp, sh, comp, check, V, ba, bb, mode)
+                assert O.max_abs_rel(got, ref) <= TOL, (sh, comp, check, s, mode)
+                assert O.max_rel_error(got, ref) <= 1e-4, (sh, comp, check, s, mode)
+
+
+def test_sparse_and_dense_modes_agree(sp):  # test_kernels.cpp:49-65
+    rng = np.random.default_rng(55)
+    for trial in range(9):
+        V = [4, 8, 16][trial % 3]
+        sh = sp.ConvShape(*rng_tiny_shape(rng, V))
+        for comp, check in ALL:
+            _, _, ba, bb = make_inputs(sp, sh, comp, check, 0.5, V, trial + 40)
+            _, _, g0 = run(sp, sh, comp, check, V, ba, bb, 0)
+            _, _, g1 = run(sp, sh, comp, check, V, ba, bb, 1)
+            assert O.max_rel_error(g0, g1) <= 1e-4
+
+
+def test_executed_fma_counters_match_simulation_exactly(sp):  # test_kernels.cpp:67-95
+    rng = np.random.default_rng(77)
+    for trial in range(30):
+        V = [4, 8, 16][trial % 3]
+        sh = sp.ConvShape(*rng_tiny_shape(rng, V))
+        s = float(rng.choice([0.0, 0.3, 0.5, 0.8, 0.9, 1.0]))
+        for comp, check in ALL:
+            a, b, ba, bb = make_inputs(sp, sh, comp, check, s, V, trial * 13 + 3)
+            pl, res, _ = run(sp, sh, comp, check, V, ba, bb, 0)
+            want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), comp, V, 30, check),
+                                     mask_of(comp, check, a, b))
+            assert res.counters.executed_vector_fmas == want["executed_vector_fmas"], (sh, comp, check, s)
+            assert res.counters.checked_vectors == want["checked_vectors"]
+            _, dres, _ = run(sp, sh, comp, check, V, ba, bb, 1)
+            assert dres.counters.executed_vector_fmas == want["dense_total"]
+            assert dres.counters.checked_vectors == 0
+
+
+def test_single_interior_nonzero_skips_everything_else(sp):  # test_kernels.cpp:97-110
+    V = 8
+    sh = sp.ConvShape.make(1, 32, 32, 8, 8, 3, 3, 1, 1)
+    D = np.zeros((1, 32, 8, 8), np.float32)
+    D[0, 5, 4, 4] = 0.7
+    G = O.gen_sparse(32, 32, 3, 3, 0.0, 2)
+    pl = sp.plan(sh, sp.Component.fwd, V)
+    res = sp.sparse_fwd(sp.pack_act_nchwc(D, V).to("cuda"), sp.pack_filter(G, V).to("cuda"), sh, pl)
+    assert res.counters.executed_vector_fmas == 36
+    got = sp.unpack(res.out).cpu().numpy()
+    assert O.max_rel_error(got, O.dense(0, sh.astuple(), D, G)) <= 1e-4
+
+
+def test_all_zero_input_runs_zero_fmas(sp):  # test_kernels.cpp:112-123
+    V = 8
+    sh = sp.ConvShape.make(2, 16, 16, 6, 6, 3, 3, 1, 1)
+    for comp, check in ALL:
+        _, _, ba, bb = make_inputs(sp, sh, comp, check, 1.0, V, 9)
+        _, res, got = run(sp, sh, comp, check, V, ba, bb, 0)
+        assert res.counters.executed_vector_fmas == 0
+        assert not got.any()
+
+
+def test_bww_single_image_outer_product(sp):  # test_kernels.cpp:125-148
+    V = 8
+    sh = sp.ConvShape.make(8, 8, 8, 1, 1, 1, 1, 1, 1)
+    D = np.zeros((8, 8, 1, 1), np.float32)
+    D[3, :, 0, 0] = np.arange(1, 9)
+    dY = O.gen_sparse(8, 8, 1, 1, 0.0, 4)
+    pl = sp.plan(sh, sp.Component.bww, V)
+    res = sp.sparse_bww(sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pl)
+    assert res.counters.executed_vector_fmas == sh.C * (sh.K // pl.Q) * (pl.Q // V)
+    dG = sp.unpack(res.out).cpu().numpy()
+    np.testing.assert_allclose(dG[:, :, 0, 0], np.outer(dY[3, :, 0, 0], D[3, :, 0, 0]), rtol=1e-6)
+
+
+def test_adding_zeros_never_increases_executed_fmas(sp):  # test_kernels.cpp:227-253
+    rng = np.random.default_rng(404)
+    V = 8
+    for trial in range(6):
+        sh = sp.ConvShape(*rng_tiny_shape(rng, V))
+        for comp, check in ALL[:3]:
+            a, b, _, bb = make_inputs(sp, sh, comp, check, 0.3, V, trial)
+            masked = a.copy()
+            prev = None
+            for step in range(4):
+                flat = masked.reshape(-1)
+                flat[rng.integers(0, flat.size, flat.size // 8)] = 0.0
+                ba = (sp.pack_act_chwnn(masked, V) if comp == 2 else sp.pack_act_nchwc(masked, V)).to("cuda")
+                _, res, _ = run(sp, sh, comp, check, V, ba, bb, 0)
+                if prev is not None:
+                    assert res.counters.executed_vector_fmas <= prev
+                prev = res.counters.executed_vector_fmas
+
+
+def test_results_are_bitwise_deterministic(sp):  # test_kernels.cpp:255-275
+    rng = np.random.default_rng(505)
+    for trial in range(8):
+        V = [4, 8, 16][trial % 3]
+        sh = sp.ConvShape(*rng_tiny_shape(rng, V))
+        for comp, check in ALL:
+            _, _, ba, bb = make_inputs(sp, sh, comp, check, 0.5, V, trial + 7)
+            _, r0, g0 = run(sp, sh, comp, check, V, ba, bb, 0)
+            for workers in (2, 4):
+                pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
+                r1 = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse, workers)
+                assert np.array_equal(sp.unpack(r1.out).cpu().numpy(), g0)
+                assert r1.counters == r0.counters
+
+
+def test_bww_check_side_selection_stays_correct(sp):  # test_kernels.cpp:300-326
+    V = 8
+    sh = sp.ConvShape.make(5, 16, 24, 6, 7, 3, 3, 1, 1)
+    D = O.gen_sparse(5, 16, 6, 7, 0.2, 1)
+    dY = O.gen_sparse(5, 24, 6, 7, 0.8, 2)
+    ref = O.dense(2, sh.astuple(), D, dY)
+    pi = sp.plan(sh, sp.Component.bww, V)
+    r = sp.sparse_bww(sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pi)
+    assert O.max_rel_error(sp.unpack(r.out).cpu().numpy(), ref) <= 1e-4
+    po = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck.output_grad)
+    r2 = sp.sparse_bww(sp.pack_act_nchwc(D, V).to("cuda"), sp.pack_act_chwnn(dY, V).to("cuda"), sh, po)
+    assert O.max_rel_error(sp.unpack(r2.out).cpu().numpy(), ref) <= 1e-4
+    assert r2.counters.executed_vector_fmas < r.counters.executed_vector_fmas
+
+
+def test_stride_wider_than_filter_leaves_gap_columns_zero(sp):  # test_kernels.cpp:354-385
+    V = 8
+    sh = sp.ConvShape.make(2, 16, 16, 7, 7, 1, 1, 2, 2)
+    for comp, check in ALL:
+        a, b, ba, bb = make_inputs(sp, sh, comp, check, 0.4, V, 61)
+        pl, res, got = run(sp, sh, comp, check, V, ba, bb, 0)
+        assert O.max_rel_error(got, O.dense(comp, sh.astuple(), a, b)) <= 1e-4
+        want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), comp, V, 30, check), mask_of(comp, check, a, b))
+        assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+    _, _, ba, bb = make_inputs(sp, sh, 1, 0, 0.0, V, 62)
+    pl, res, dD = run(sp, sh, 1, 0, V, ba, bb, 0)
+    assert not dD[:, :, :, 1::2].any() and not dD[:, :, 1::2, :].any()
+    sweeps = 4 * (sh.K // V) * sh.N * (sh.C // pl.Q)
+    assert res.counters.output_vector_loads == sweeps * 4 * (pl.Q // V)
+    assert res.counters.output_vector_stores == sweeps * 4 * (pl.Q // V)
+
+
+def test_strided_geometries_match_oracle(sp):  # test_kernels.cpp:407-422
+    V = 8
+    sh = sp.ConvShape.make(2, 16, 16, 14, 14, 3, 3, 2, 2)
+    for comp, check in ALL:
+        a, b, ba, bb = make_inputs(sp, sh, comp, check, 0.5, V, 21)
+        _, res, got = run(sp, sh, comp, check, V, ba, bb, 0)
+        assert O.max_rel_error(got, O.dense(comp, sh.astuple(), a, b)) <= 1e-4
+        want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), comp, V, 30, check), mask_of(comp, check, a, b))
+        assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+
+
+def test_negative_zero_is_skipped_nan_inf_participate(sp):  # vec.hpp:120-128, README "Notes"
+    V = 16
+    sh = sp.ConvShape.make(1, 16, 16, 4, 4, 3, 3, 1, 1)
+    D = np.zeros((1, 16, 4, 4), np.float32)
+    D[0, 0, 1, 1] = -0.0
+    D[0, 3, 2, 2] = 1.5
+    G = O.gen_sparse(16, 16, 3, 3, 0.0, 5)
+    pl = sp.plan(sh, sp.Component.fwd, V)
+    r = sp.sparse_fwd(sp.pack_act_nchwc(D, V).to("cuda"), sp.pack_filter(G, V).to("cuda"), sh, pl)
+    assert r.counters.executed_vector_fmas == O.expected_counts(sh.astuple(), O.plan(sh.astuple(), 0, V), D)[
+        "executed_vector_fmas"] == 9  # only the 1.5 (9 taps x K/V=1)
+    D[0, 7, 0, 0] = math.nan
+    D[0, 8, 3, 3] = math.inf
+    r = sp.sparse_fwd(sp.pack_act_nchwc(D, V).to("cuda"), sp.pack_filter(G, V).to("cuda"), sh, pl)
+    y = sp.unpack(r.out).cpu().numpy()
+    ref = O.dense(0, sh.astuple(), D, G)
+    assert np.array_equal(np.isnan(y), np.isnan(ref))
+    assert np.array_equal(np.isinf(y), np.isinf(ref))
+    fin = np.isfinite(ref)
+    assert O.max_abs_rel(y[fin], ref[fin]) <= TOL
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=lambda p: os.path.basename(p)[:-4])
+def test_golden_fixtures_from_reference(sp, path):
+    """Byte-identical operands the reference packed -> our kernels -> compare
+    with the reference CPU kernel's output, its counters and the 64-bit oracle."""
+    import torch
+    z = np.load(path)
+    sh = sp.ConvShape(*[int(v) for v in z["shape"]])
+    V = int(z["V"])
+    for comp, check, tag in [(0, 0, "fwd"), (1, 0, "bwi"), (2, 0, "bww_in"), (2, 1, "bww_og")]:
+        a, b = z[f"{tag}_a"], z[f"{tag}_b"]
+        if comp == 0:
+            ba, bb = sp.pack_act_nchwc(a, V), sp.pack_filter(b, V)
+        elif comp == 1:
+            ba, bb = sp.pack_act_nchwc(a, V), sp.pack_filter(b, V, True)
+        elif check == 0:
+            ba, bb = sp.pack_act_chwnn(a, V), sp.pack_act_nchwc(b, V)
+        else:
+            ba, bb = sp.pack_act_nchwc(a, V), sp.pack_act_chwnn(b, V)
+        assert np.array_equal(ba.data, z[f"{tag}_a_blk"]) and np.array_equal(bb.data, z[f"{tag}_b_blk"])
+        ba.data, bb.data = torch.from_numpy(z[f"{tag}_a_blk"]).cuda(), torch.from_numpy(z[f"{tag}_b_blk"]).cuda()
+        for mode, ckey in ((0, "sparse"), (1, "dense")):
+            _, res, got = run(sp, sh, comp, check, V, ba, bb, mode)
+            assert O.max_abs_rel(got, z[f"{tag}_oracle64"]) <= TOL, (tag, mode)
+            assert O.max_abs_rel(got, z[f"{tag}_ref_{'sparse' if mode == 0 else 'dense_mode'}"]) <= 2 * TOL
+            c = z[f"{tag}_counters_{ckey}"]
+            assert [res.counters.checked_vectors, res.counters.executed_vector_fmas,
+                    res.counters.output_vector_loads, res.counters.output_vector_stores] == [int(v) for v in c], tag
+
+
+def test_host_buffer_dropin_matches_device_path(sp):
+    """spc_run_parallel_host (numpy in, numpy out) == the device path, bitwise."""
+    V = 16
+    sh = sp.ConvShape.make(3, 32, 48, 9, 11, 3, 3, 1, 1)
+    for comp, check in ALL:
+        a, b, ba, bb = make_inputs(sp, sh, comp, check, 0.5, V, 5)
+        pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
+        rd = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse)
+        rh = sp.run_parallel(ba.to(None), bb.to(None), sh, pl, sp.RunMode.sparse)
+        assert isinstance(rh.out.data, np.ndarray)
+        assert np.array_equal(rh.out.data, rd.out.data.cpu().numpy())
+        assert rh.counters == rd.counters
+
+
+def test_relu_and_grad_mask_bit_exact(sp):
+    import torch
+    x = np.array([-1.0, -0.0, 0.0, 2.5, math.nan, math.inf, -math.inf, 1e-38, -1e-45, 3.0], np.float32)
+    x = np.tile(x, 1000)
+    up = np.arange(x.size, dtype=np.float32) - 7
+    r = sp.relu_(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(r.view(np.uint32), O.relu(x).view(np.uint32))
+    m = sp.relu_grad_mask(torch.from_numpy(x).cuda(), torch.from_numpy(up).cuda()).cpu().numpy()
+    assert np.array_equal(m.view(np.uint32), O.relu_grad_mask(x, up).view(np.uint32))
+
+
+def test_device_chwnn_transpose_matches_pack(sp):
+    import torch
+    rng = np.random.default_rng(3)
+    for V, n in ((16, 19), (8, 8), (4, 3)):
+        t = rng.standard_normal((n, 2 * V, 5, 6)).astype(np.float32)
+        src = sp.pack_act_nchwc(t, V).to("cuda")
+        got = sp.nchwc_to_chwnn(src)
+        assert np.array_equal(got.data.cpu().numpy(), O.pack_act(t, V, chwnn=True))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("comp,check", ALL)
+def test_config1_full_size_matches_reference_cpu(sp, comp, check):
+    """BASELINE config 1 (N=16, C=K=64, 56x56, 3x3) at full size: GPU vs the
+    reference's own CPU kernel on identical seeded inputs, values within TOL
+    of max-abs and FMA counters exact; plus a 64-bit oracle check on an image slice."""
+    from paper_1911_10175_b200 import workloads as wl
+    V = 16
+    sh = sp.ConvShape.make(16, 64, 64, 56, 56, 3, 3, 1, 1)
+    D, G, dY = wl.config1_inputs_host(seed=0)
+    a, b = {0: (D, G), 1: (dY, G), 2: (D, dY)}[comp]
+    r = O.RefRun(comp, check, sh.astuple(), V, a, b)
+    r.exec(0, os.cpu_count() or 1)
+    ref_out, ref_cnt, _ = r.result()
+    import torch
+    ba, bb = torch.from_numpy(r.operand(0)).cuda(), torch.from_numpy(r.operand(1)).cuda()
+    lay = {0: (sp.Layout.act_nchwc, sp.Layout.filter_kcrs_blk), 1: (sp.Layout.act_nchwc, sp.Layout.filter_kcrs_blk),
+           2: ((sp.Layout.act_chwnn, sp.Layout.act_nchwc) if check == 0 else (sp.Layout.act_nchwc, sp.Layout.act_chwnn))}[comp]
+    ta = sp.BlockedTensor(lay[0], V, sh.N, sh.C if comp != 1 else sh.K, sh.H if comp != 1 else sh.out_h(),
+                          sh.W if comp != 1 else sh.out_w(), data=ba)
+    if comp == 2:
+        tb = sp.BlockedTensor(lay[1], V, sh.N, sh.K, sh.out_h(), sh.out_w(), data=bb)
+    else:
+        tb = sp.BlockedTensor(lay[1], V, k=sh.K if comp == 0 else sh.C, c=sh.C if comp == 0 else sh.K,
+                              s=sh.S, r=sh.R, data=bb)
+    _, res, got = run(sp, sh, comp, check, V, ta, tb, 0)
+    assert O.max_abs_rel(got, ref_out) <= TOL
+    assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
+    assert res.counters.checked_vectors == ref_cnt["checked_vectors"]
+    # 64-bit oracle on a 2-image slice (FWD/BWI are per-image independent)
+    if comp in (0, 1):
+        sl = sh.with_batch(2).astuple()
+        ref2 = O.dense(comp, sl, a[:2], b)
+        assert O.max_abs_rel(got[:2], ref2) <= TOL
