@@ -151,6 +151,14 @@ int spc_abi_version(void);
 /* Count of device kernels this library has launched in this process. */
 uint64_t spc_launch_count(void);
 
+/* ---- measurement support (not part of the reference interface) ---- */
+/* FP32 FFMA-pipe peak probe: launches `blocks` CTAs of 256 threads, each
+ * thread running `iters` x 16 independent FFMAs; out[0] receives a checksum.
+ * Returns the kernel's FLOP count in *flops (time it with events). */
+spc_status spc_ffma_peak_kernel(float* out, int blocks, int iters, double* flops, void* stream);
+/* Write `n` floats of scratch (an L2 flush between timed steps). */
+spc_status spc_l2_flush(float* scratch, size_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

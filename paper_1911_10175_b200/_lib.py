@@ -65,6 +65,8 @@ _SIGS = {
     "spc_relu": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_relu_grad_mask": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_nchwc_to_chwnn": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.c_void_p]),
+    "spc_ffma_peak_kernel": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_void_p]),
+    "spc_l2_flush": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
 }
 
 # Every symbol include/spconv_b200.h declares (checked by the CPU test suite).

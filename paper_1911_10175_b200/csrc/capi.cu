@@ -377,6 +377,27 @@ __global__ void nchwc_to_chwnn_kernel(const float* __restrict__ src, float* __re
     }
 }
 
+// FFMA peak probe: 16 independent accumulator chains per thread.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters) {
+    float a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = threadIdx.x * 1e-7f + j;
+    const float b = 0.999999f, c = 1e-7f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = fmaf(a[j], b, c);
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s += a[j];
+    if (s == 12345.678f) out[0] = s;  // keeps the chains live
+}
+
+__global__ void l2_flush_kernel(float* p, size_t n) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+        p[e] = (float)e;
+}
+
 static unsigned grid_for(size_t n) {
     size_t b = (n + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
@@ -585,6 +606,27 @@ spc_status spc_relu_grad_mask(const float* pre, const float* upstream, float* ou
     note_launch();
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SPC_OK : cuda_fail(e, "relu_grad_mask");
+}
+
+spc_status spc_ffma_peak_kernel(float* out, int blocks, int iters, double* flops, void* stream) {
+    if (!out || blocks < 1 || iters < 1) return fail(SPC_ERR_ARG, "bad argument");
+    spc_status st = check_device();
+    if (st) return st;
+    ffma_peak_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(out, iters);
+    note_launch();
+    if (flops) *flops = 2.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "ffma peak");
+}
+
+spc_status spc_l2_flush(float* scratch, size_t n, void* stream) {
+    if (!scratch) return fail(SPC_ERR_ARG, "null scratch");
+    spc_status st = check_device();
+    if (st) return st;
+    l2_flush_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(scratch, n);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "l2 flush");
 }
 
 spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stream) {

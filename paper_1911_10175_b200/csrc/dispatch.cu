@@ -1,15 +1,27 @@
 // dispatch.cu -- kernel selection (internal).
 #include "dispatch.h"
 
+#include <cstdlib>
+
+#include "tile_bww.h"
+#include "tile_conv.h"
+
 namespace spc {
 
 cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,
                         float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    // SPC_FORCE_GENERIC=1 selects the shape-general kernels (A/B testing only)
+    static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
+    if (!force_generic && tile_conv_supported(fwd, sh, V))
+        return launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st);
     return launch_conv_generic(fwd, sparse, sh, V, src, filt, dst, exec_ctr, st);
 }
 
 cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V, const float* chk,
                        const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
+    if (!force_generic && tile_bww_supported(check_input, sh, V))
+        return launch_tile_bww(check_input, sparse, sh, chk, oth, dst, exec_ctr, st);
     const int splits = bww_generic_splits(sh);
     const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
     float* partial = nullptr;

@@ -1,0 +1,440 @@
+// tile_bww.cu -- tuned sm_100a BWW kernels for V = 16 blocked layouts.
+//
+// dG[k,c,v,u] = sum_{i,y',x'} D[i,c,y'P+v-padH, x'O+u-padW] * dY[i,k,y',x']
+// (P/src/kernel_impl.hpp:209-336, P/src/kernels.cpp:238-302).
+//
+// The checked tensor arrives in ActCHWNn ([N/16][C][H][W][16 images]) as the
+// reference's API requires.  A CTA of NWC warps owns one output-pixel tile,
+// 32*KK lane channels (the OTHER tensor's channels, KK per lane) and NWC*CB
+// checked channels (CB per warp).  The checked region of those channels is
+// staged in shared memory with 4-byte cp.async that transposes the 16-image
+// vectors into per-(channel, image) pixel planes, so for one image:
+//   * one conflict-free lane load + __ballot_sync gives the nonzero mask of 32
+//     region pixels (warp-uniform: every lane consumes the same checked value,
+//     `d != 0.0f`, -0 is zero and NaN is not, P/include/spconv/vec.hpp:120-128);
+//   * each region row's values arrive by broadcast 128-bit loads, one row ahead
+//     of the uniform branches that skip the FMAs a zero would have fed.
+// The other operand's pixel tile for the current image sits in registers and
+// is reused by all CB channels x R*S taps of the warp; the NWC warps load the
+// same tile, so L1 serves all but the first.  Accumulators (CB x R*S x KK) are
+// register-resident for the whole reduction -- no per-FMA reloads (the CPU
+// BWW's bottleneck).
+//
+// check = input:       checked = D  (input pixels, halo'd region), other = dY tile
+// check = output_grad: checked = dY (output tile),                  other = D region
+//
+// The reduction over images and pixels is split over CTAs (fixed item ranges);
+// bww_tile_reduce sums the splits in fixed order: bitwise deterministic, no
+// float atomics.  The final store writes FilterKCRSblk (K, C) for either check
+// side, i.e. the reference's check=output_grad transpose (kernels.cpp:285-300)
+// is fused into the reduction.
+#include "common.cuh"
+#include "tile_bww.h"
+
+namespace spc {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int KK>
+__device__ __forceinline__ void ld_vec(float (&o)[KK], const float* p) {
+    if constexpr (KK == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+    } else if constexpr (KK == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __ldg(p);
+    }
+}
+
+}  // namespace
+
+template <bool CHECK_INPUT, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR>
+struct BwwGeom {
+    static constexpr int PADH = (S - 1) / 2, PADW = (R - 1) / 2;
+    static constexpr int TAPS = R * S;
+    static constexpr int IRH = (TH - 1) * STR + S;  // input-pixel region of the output tile
+    static constexpr int IRW = (TW - 1) * STR + R;
+    static constexpr int CRH = CHECK_INPUT ? IRH : TH;  // checked region
+    static constexpr int CRW = CHECK_INPUT ? IRW : TW;
+    static constexpr int NQ = (CRW + 3) / 4;
+    static constexpr int CRWP = NQ * 4;
+    static constexpr int PLANE = CRH * CRWP;          // one (channel, image) plane
+    static constexpr int CHW = CRH * CRW;
+    static constexpr int NWORD = (CHW + 31) / 32;
+    static constexpr int OTH = CHECK_INPUT ? TH : IRH;  // other-operand register tile
+    static constexpr int OTW = CHECK_INPUT ? TW : IRW;
+    static constexpr int NCH = NWC * CB;               // checked channels per CTA
+    static constexpr int NT = NWC * 32;
+    static constexpr int NST = 4;                      // pipeline stages (one image each)
+    static constexpr int CFLOATS = NCH * PLANE;         // checked planes of one image
+    static constexpr int OFLOATS = OTH * OTW * 32 * KK;  // other tile of one image
+    static constexpr int STAGE = CFLOATS + OFLOATS;
+    static constexpr int SMEM = NST * STAGE * 4;
+};
+
+template <bool CHECK_INPUT, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, bool SPARSE>
+__global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const float* __restrict__ chk,
+                                                            const float* __restrict__ oth,
+                                                            float* __restrict__ partial, int splits,
+                                                            unsigned long long* __restrict__ exec_ctr) {
+    using G = BwwGeom<CHECK_INPUT, KK, CB, NWC, TH, TW, R, S, STR>;
+    constexpr int TAPS = G::TAPS, CRH = G::CRH, CRW = G::CRW, CRWP = G::CRWP, PLANE = G::PLANE;
+    constexpr int CHW = G::CHW, NWORD = G::NWORD, NQ = G::NQ, OTH = G::OTH, OTW = G::OTW, NCH = G::NCH;
+
+    extern __shared__ __align__(16) float smem[];  // NST x {checked [NCH][CRH][CRWP], other [OTH*OTW][32*KK]}
+
+    const int Lc = CHECK_INPUT ? sh.K : sh.C;  // lane channels (other tensor)
+    const int Mc = CHECK_INPUT ? sh.C : sh.K;  // checked channels
+    const int Hc = CHECK_INPUT ? sh.H : sh.Hp, Wc = CHECK_INPUT ? sh.W : sh.Wp;  // checked dims
+    const int Ho = CHECK_INPUT ? sh.Hp : sh.H, Wo = CHECK_INPUT ? sh.Wp : sh.W;  // other dims
+    const int LcB = Lc / 16;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mc0 = blockIdx.x * NCH;        // first checked channel of the CTA
+    const int lc0 = blockIdx.y * 32 * KK;    // first lane channel of the CTA
+    const int l0 = lc0 + lane * KK;          // this lane's first lane channel
+
+    const int tiles_x = (sh.Wp + TW - 1) / TW;
+    const int ntiles = tiles_x * ((sh.Hp + TH - 1) / TH);
+    const int nb = (sh.N + 15) / 16;
+    const long items = (long)nb * ntiles;
+    const long it0 = items * blockIdx.z / splits, it1 = items * (blockIdx.z + 1) / splits;
+
+    float acc[CB][TAPS][KK];
+#pragma unroll
+    for (int a = 0; a < CB; ++a)
+#pragma unroll
+        for (int f = 0; f < TAPS; ++f)
+#pragma unroll
+            for (int j = 0; j < KK; ++j) acc[a][f][j] = 0.0f;
+
+    auto origin = [&](long it, int& ib, int& y0, int& x0) {
+        ib = (int)(it / ntiles);
+        const int t = (int)(it % ntiles);
+        y0 = (t / tiles_x) * TH;
+        x0 = (t % tiles_x) * TW;
+    };
+    auto nimg_of = [&](long it) { return min(16, sh.N - (int)(it / ntiles) * 16); };
+
+    // One pipeline stage = one (item, image): the checked planes of that image
+    // (4-byte cp.async out of the 16-image CHWNn vectors; .ca keeps the lines in
+    // L1 for the item's other images) and the other operand's pixel tile
+    // ([pixel][32*KK lane channels], 16-byte cp.async).
+    auto stage = [&](long it, int j, int buf) {
+        int ib, y0, x0;
+        origin(it, ib, y0, x0);
+        float* base = smem + buf * G::STAGE;
+        const uint32_t dc = smem_u32(base);
+        const int cy0 = CHECK_INPUT ? y0 * STR - G::PADH : y0;
+        const int cx0 = CHECK_INPUT ? x0 * STR - G::PADW : x0;
+        for (int idx = threadIdx.x; idx < NCH * CRH * CRW; idx += NWC * 32) {
+            const int rx = idx % CRW;
+            const int ry = (idx / CRW) % CRH;
+            const int cc = idx / (CRW * CRH);
+            const int gy = cy0 + ry, gx = cx0 + rx;
+            const bool ok = gy >= 0 && gy < Hc && gx >= 0 && gx < Wc;
+            const float* g = ok ? chk + ((((size_t)ib * Mc + mc0 + cc) * Hc + gy) * Wc + gx) * 16 + j : chk;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                             dc + (uint32_t)(cc * PLANE + ry * CRWP + rx) * 4u),
+                         "l"(g), "r"(ok ? 4 : 0));
+        }
+        const int oy0 = CHECK_INPUT ? y0 : y0 * STR - G::PADH;
+        const int ox0 = CHECK_INPUT ? x0 : x0 * STR - G::PADW;
+        const int i = ib * 16 + j;
+        const uint32_t doo = smem_u32(base + G::CFLOATS);
+        for (int idx = threadIdx.x; idx < OTH * OTW * 8 * KK; idx += NWC * 32) {
+            const int c4 = idx % (8 * KK), q = idx / (8 * KK);
+            const int gy = oy0 + q / OTW, gx = ox0 + q % OTW;
+            const int ch = lc0 + c4 * 4;
+            const bool ok = gy >= 0 && gy < Ho && gx >= 0 && gx < Wo;
+            const float* g =
+                ok ? oth + ((((size_t)i * LcB + ch / 16) * Ho + gy) * Wo + gx) * 16 + (ch % 16) : oth;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(doo + (uint32_t)idx * 16u),
+                         "l"(g), "r"(ok ? 16 : 0));
+        }
+    };
+
+    // lane pixel offsets inside a plane (fixed for every item)
+    int qoff[NWORD];
+#pragma unroll
+    for (int w = 0; w < NWORD; ++w) {
+        const int q = lane + 32 * w;
+        qoff[w] = q < CHW ? (q / CRW) * CRWP + q % CRW : 0;
+    }
+    uint32_t cnt = 0;
+
+    // prefetch cursor runs NST-1 stages ahead of the consumer
+    long pit = it0;
+    int pj = 0;
+    auto advance = [&](long& it, int& j) {
+        if (++j >= nimg_of(it)) {
+            j = 0;
+            ++it;
+        }
+    };
+    for (int d = 0; d < G::NST - 1; ++d) {
+        if (pit < it1) {
+            stage(pit, pj, d);
+            advance(pit, pj);
+        }
+        cp_async_commit();
+    }
+    int ord = 0;
+    for (long it = it0; it < it1; ++it) {
+        int ib, y0, x0;
+        origin(it, ib, y0, x0);
+        const int nimg = nimg_of(it);
+
+        // valid (tap, partner) weight of this lane's checked pixels, for counting
+        uint32_t wt[NWORD];
+#pragma unroll
+        for (int w = 0; w < NWORD; ++w) {
+            const int q = lane + 32 * w;
+            uint32_t ny = 0, nx = 0;
+            if (q < CHW) {
+                const int ry = q / CRW, rx = q % CRW;
+                if (CHECK_INPUT) {  // (tap, output pixel) pairs with the output inside the image
+#pragma unroll
+                    for (int v = 0; v < S; ++v) {
+                        const int num = ry - v;
+                        if (num >= 0 && num % STR == 0 && num / STR < TH && y0 + num / STR < sh.Hp) ++ny;
+                    }
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        const int num = rx - u;
+                        if (num >= 0 && num % STR == 0 && num / STR < TW && x0 + num / STR < sh.Wp) ++nx;
+                    }
+                } else if (y0 + ry < sh.Hp && x0 + rx < sh.Wp) {  // taps whose input pixel is inside
+#pragma unroll
+                    for (int v = 0; v < S; ++v) {
+                        const int y = (y0 + ry) * STR + v - G::PADH;
+                        if (y >= 0 && y < sh.H) ++ny;
+                    }
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        const int x = (x0 + rx) * STR + u - G::PADW;
+                        if (x >= 0 && x < sh.W) ++nx;
+                    }
+                }
+            }
+            wt[w] = ny * nx;
+        }
+
+#pragma unroll 1
+        for (int j = 0; j < nimg; ++j, ++ord) {
+            if (pit < it1) {
+                stage(pit, pj, (ord + G::NST - 1) % G::NST);
+                advance(pit, pj);
+            }
+            cp_async_commit();
+            cp_async_wait<G::NST - 1>();
+            __syncthreads();
+
+            const float* base = smem + (ord % G::NST) * G::STAGE;
+            float O[OTH * OTW][KK];
+            const float* Ob = base + G::CFLOATS + lane * KK;
+#pragma unroll
+            for (int q = 0; q < OTH * OTW; ++q) {
+                if constexpr (KK == 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(Ob + q * 32 * KK);
+                    O[q][0] = t.x; O[q][1] = t.y; O[q][2] = t.z; O[q][3] = t.w;
+                } else if constexpr (KK == 2) {
+                    const float2 t = *reinterpret_cast<const float2*>(Ob + q * 32 * KK);
+                    O[q][0] = t.x; O[q][1] = t.y;
+                } else {
+                    O[q][0] = Ob[q * 32 * KK];
+                }
+            }
+#pragma unroll
+            for (int cc = 0; cc < CB; ++cc) {
+                const float* Pl = base + (warp * CB + cc) * PLANE;
+                uint32_t m[NWORD];
+                if (SPARSE) {
+#pragma unroll
+                    for (int w = 0; w < NWORD; ++w) {
+                        const bool nz = (lane + 32 * w < CHW) && Pl[qoff[w]] != 0.0f;
+                        cnt += nz ? wt[w] : 0u;
+                        m[w] = __ballot_sync(0xffffffffu, nz);
+                    }
+                }
+                float4 cur[NQ], nxt[NQ];
+#pragma unroll
+                for (int h = 0; h < NQ; ++h) cur[h] = *reinterpret_cast<const float4*>(Pl + 4 * h);
+#pragma unroll
+                for (int ry = 0; ry < CRH; ++ry) {
+                    if (ry + 1 < CRH) {
+#pragma unroll
+                        for (int h = 0; h < NQ; ++h)
+                            nxt[h] = *reinterpret_cast<const float4*>(Pl + (ry + 1) * CRWP + 4 * h);
+                    }
+#pragma unroll
+                    for (int rx = 0; rx < CRW; ++rx) {
+                        const int p = ry * CRW + rx;
+                        if (!SPARSE || ((m[p >> 5] >> (p & 31)) & 1u)) {
+                            const float4 q4 = cur[rx >> 2];
+                            const float d =
+                                (rx & 3) == 0 ? q4.x : (rx & 3) == 1 ? q4.y : (rx & 3) == 2 ? q4.z : q4.w;
+#pragma unroll
+                            for (int v = 0; v < S; ++v) {
+#pragma unroll
+                                for (int u = 0; u < R; ++u) {
+                                    int q;
+                                    if (CHECK_INPUT) {
+                                        const int ny = ry - v, nx = rx - u;
+                                        if (ny < 0 || nx < 0 || ny % STR || nx % STR || ny / STR >= TH ||
+                                            nx / STR >= TW)
+                                            continue;
+                                        q = (ny / STR) * OTW + nx / STR;
+                                    } else {
+                                        q = (ry * STR + v) * OTW + rx * STR + u;
+                                    }
+#pragma unroll
+                                    for (int jj = 0; jj < KK; ++jj)
+                                        acc[cc][v * R + u][jj] = fmaf(d, O[q][jj], acc[cc][v * R + u][jj]);
+                                }
+                            }
+                        }
+                    }
+                    if (ry + 1 < CRH) {
+#pragma unroll
+                        for (int h = 0; h < NQ; ++h) cur[h] = nxt[h];
+                    }
+                }
+            }
+            __syncthreads();  // stage buffer free for reuse
+        }
+    }
+    cp_async_wait<0>();
+
+    // partial[z][m][tap][l]: warps own disjoint checked channels
+    float* pz = partial + (size_t)blockIdx.z * Mc * TAPS * Lc;
+#pragma unroll
+    for (int a = 0; a < CB; ++a)
+#pragma unroll
+        for (int f = 0; f < TAPS; ++f) {
+            float* dstp = pz + ((size_t)(mc0 + warp * CB + a) * TAPS + f) * Lc + l0;
+            if constexpr (KK == 4) {
+                *reinterpret_cast<float4*>(dstp) = make_float4(acc[a][f][0], acc[a][f][1], acc[a][f][2], acc[a][f][3]);
+            } else if constexpr (KK == 2) {
+                *reinterpret_cast<float2*>(dstp) = make_float2(acc[a][f][0], acc[a][f][1]);
+            } else {
+                dstp[0] = acc[a][f][0];
+            }
+        }
+    if (SPARSE && exec_ctr) {
+        const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0 && total) atomicAdd(exec_ctr, (unsigned long long)total * (2 * KK));
+    }
+}
+
+// Sum the splits in fixed order and scatter into FilterKCRSblk (K, C).
+template <bool CHECK_INPUT>
+__global__ void bww_tile_reduce(DevShape sh, const float* __restrict__ partial, int splits, float* __restrict__ dst) {
+    const int TAPS = sh.R * sh.S;
+    const int Lc = CHECK_INPUT ? sh.K : sh.C, Mc = CHECK_INPUT ? sh.C : sh.K;
+    const size_t E = (size_t)Mc * TAPS * Lc;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < E; e += (size_t)gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int z = 0; z < splits; ++z) s += partial[(size_t)z * E + e];
+        const int l = (int)(e % Lc);
+        const int f = (int)((e / Lc) % TAPS);
+        const int m = (int)(e / ((size_t)Lc * TAPS));
+        const int k = CHECK_INPUT ? l : m, c = CHECK_INPUT ? m : l;
+        dst[filter_index(sh.C, sh.S, sh.R, 16, k, c, f % sh.R, f / sh.R)] = s;
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+template <bool CI, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR>
+static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* chk, const float* oth,
+                                  float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    using G = BwwGeom<CI, KK, CB, NWC, TH, TW, R, S, STR>;
+    const int Lc = CI ? sh.K : sh.C, Mc = CI ? sh.C : sh.K;
+    const long items = (long)((sh.N + 15) / 16) * ((sh.Wp + TW - 1) / TW) * ((sh.Hp + TH - 1) / TH);
+    const long base = (long)(Mc / G::NCH) * (Lc / (32 * KK));
+    long splits = (148L * 6 + base - 1) / base;
+    if (splits > items) splits = items;
+    if (splits < 1) splits = 1;
+    const size_t E = (size_t)Mc * R * S * Lc;
+    float* partial = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)splits * E * sizeof(float), st);
+    if (e != cudaSuccess) return e;
+    dim3 grid(Mc / G::NCH, Lc / (32 * KK), (unsigned)splits);
+    auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, true>
+                       : bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    kern<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr);
+    note_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        unsigned rb = (unsigned)((E + 255) / 256);
+        if (rb > 148 * 8) rb = 148 * 8;
+        bww_tile_reduce<CI><<<rb, 256, 0, st>>>(sh, partial, (int)splits, dst);
+        note_launch();
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(partial, st);
+    return e;
+}
+
+bool tile_bww_supported(bool check_input, const DevShape& sh, int V) {
+    if (V != 16) return false;
+    const int Lc = check_input ? sh.K : sh.C, Mc = check_input ? sh.C : sh.K;
+    if (Lc % 64 || Mc % 16) return false;
+    if (sh.R != sh.S || sh.O != sh.P) return false;
+    if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
+    if ((sh.R == 3 || sh.R == 1) && (sh.O == 1 || sh.O == 2)) return true;
+    return false;
+}
+
+cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, const float* chk, const float* oth,
+                            float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    const int Lc = check_input ? sh.K : sh.C;
+    const bool kk4 = Lc % 128 == 0;
+#define SPC_B(CI, KK, CB, NWC, TH, TW, R, STR) \
+    return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, STR>(sparse, sh, chk, oth, dst, exec_ctr, st)
+    if (check_input) {
+        if (sh.R == 3 && sh.O == 1) {
+            if (kk4) SPC_B(true, 4, 2, 4, 4, 4, 3, 1);
+            SPC_B(true, 2, 4, 4, 4, 4, 3, 1);
+        }
+        if (sh.R == 3) {
+            if (kk4) SPC_B(true, 4, 2, 4, 2, 4, 3, 2);
+            SPC_B(true, 2, 4, 4, 2, 4, 3, 2);
+        }
+        if (sh.O == 1) {
+            if (kk4) SPC_B(true, 4, 4, 4, 4, 8, 1, 1);
+            SPC_B(true, 2, 4, 4, 4, 8, 1, 1);
+        }
+        if (kk4) SPC_B(true, 4, 4, 4, 4, 8, 1, 2);
+        SPC_B(true, 2, 4, 4, 4, 8, 1, 2);
+    }
+    if (sh.R == 3 && sh.O == 1) {
+        if (kk4) SPC_B(false, 4, 2, 4, 2, 4, 3, 1);
+        SPC_B(false, 2, 2, 4, 4, 4, 3, 1);
+    }
+    if (sh.R == 3) {
+        if (kk4) SPC_B(false, 4, 2, 4, 2, 2, 3, 2);
+        SPC_B(false, 2, 2, 4, 2, 4, 3, 2);
+    }
+    if (sh.O == 1) {
+        if (kk4) SPC_B(false, 4, 4, 4, 4, 8, 1, 1);
+        SPC_B(false, 2, 4, 4, 4, 8, 1, 1);
+    }
+    if (kk4) SPC_B(false, 4, 4, 4, 4, 8, 1, 2);
+    SPC_B(false, 2, 4, 4, 4, 8, 1, 2);
+#undef SPC_B
+}
+
+}  // namespace spc

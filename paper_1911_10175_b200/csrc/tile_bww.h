@@ -1,0 +1,9 @@
+// tile_bww.h -- tuned V=16 BWW tile kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace spc {
+bool tile_bww_supported(bool check_input, const DevShape& sh, int V);
+cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, const float* chk, const float* oth,
+                            float* dst, unsigned long long* exec_ctr, cudaStream_t st);
+}  // namespace spc

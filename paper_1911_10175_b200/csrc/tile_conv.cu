@@ -1,0 +1,387 @@
+// tile_conv.cu -- tuned sm_100a FWD / BWI kernels for V = 16 blocked layouts.
+//
+// The GPU restatement of the paper's K-vectorised sparse row sweep
+// (P/src/kernel_impl.hpp:51-202, Alg. 2-3):
+//
+//   * lanes own OUTPUT channels (KK consecutive channels per lane, 32*KK per
+//     warp) -- the paper's "vectorise along K" -- so every lane consumes the
+//     same checked element d and the zero test is warp-uniform: one
+//     __ballot_sync per 32 region pixels per channel replaces the per-vector
+//     compare (vec.hpp:120-128), and a uniform branch skips all R*S*KK FMAs
+//     a zero would have fed (`d != 0.0f`: -0 is zero, NaN is not);
+//   * each warp keeps a TH x TW output tile x KK channels in registers for the
+//     whole reduction (the ring of kernel_impl.hpp:110-157 becomes a static
+//     register tile: outputs are written exactly once, never re-read);
+//   * the swept tensor's region for one 16-channel block is staged in shared
+//     memory with cp.async (double-buffered across channel blocks, 128-bit
+//     transfers, zero-filled virtual padding), filters stream through L1 with
+//     128/64-bit loads, prefetched one channel ahead;
+//   * BWI runs the same body with channel roles swapped, the transposed filter
+//     (pack_filter swap_kc) and the inverse spatial map (kernel_impl.hpp:85-89).
+//
+// Exact skip accounting (kernel_counters::executed_vector_fmas): every lane
+// adds popcount(its pixel's 16-channel nonzero mask) x (valid output taps of
+// that pixel) per channel block; the warp total x (2*KK vectors) is the
+// reference's count (P/src/kernel_impl.hpp:188-189) independent of tiling.
+#include "common.cuh"
+#include "tile_conv.h"
+
+namespace spc {
+
+__host__ __device__ constexpr int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int KK>
+struct FVec;
+template <>
+struct FVec<2> {
+    float v[2];
+    __device__ __forceinline__ void load(const float* p) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = t.x; v[1] = t.y;
+    }
+    __device__ __forceinline__ void store(float* p) const { *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]); }
+};
+template <>
+struct FVec<4> {
+    float v[4];
+    __device__ __forceinline__ void load(const float* p) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+    __device__ __forceinline__ void store(float* p) const {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+
+// Static geometry of one warp tile.  Target = output of the pass (Y for FWD,
+// dD for BWI); source = the swept tensor (D for FWD, dY for BWI).
+template <bool FWD, int T, int F, int STR>  // T = tile extent, F = filter extent
+struct Axis {
+    static constexpr int PAD = (F - 1) / 2;
+    // first source coordinate of the region relative to (tile origin mapped)
+    static constexpr int R0 = FWD ? 0 : fdiv(PAD - (F - 1), STR);
+    static constexpr int EXT = FWD ? (T - 1) * STR + F : fdiv(T - 1 + PAD, STR) - R0 + 1;
+    // target index fed by region coordinate r through filter tap f, or -1
+    __host__ __device__ static constexpr int target(int r, int f) {
+        if (FWD) {
+            const int num = r - f;
+            if (num < 0 || num % STR) return -1;
+            return num / STR < T ? num / STR : -1;
+        } else {
+            const int t = (R0 + r) * STR + f - PAD;
+            return (t >= 0 && t < T) ? t : -1;
+        }
+    }
+};
+
+// One CTA = NWY x NWX warps; each warp owns a TH x TW output tile x 32*KK
+// output channels (the CTA's channel group).  All warps share the staged
+// source region and read the same filter lines (L1 hits after the first).
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR>
+struct ConvGeom {
+    using AY = Axis<FWD, TH, S, STR>;
+    using AX = Axis<FWD, TW, R, STR>;
+    static constexpr int RH = AY::EXT, RWW = AX::EXT;         // one warp's region
+    static constexpr int YSTEP = FWD ? TH * STR : TH / STR;   // region offset between warp tiles
+    static constexpr int XSTEP = FWD ? TW * STR : TW / STR;
+    static constexpr int NQ = (RWW + 3) / 4;                  // float4 chunks per warp region row
+    static constexpr int CRH = (NWY - 1) * YSTEP + RH;         // CTA region
+    static constexpr int CRW = (NWX - 1) * XSTEP + RWW;
+    static constexpr int CRWP = ((NWX - 1) * XSTEP + 4 * NQ + 3) / 4 * 4;  // padded row (16B multiple)
+    static constexpr int PLANE = CRH * CRWP;
+    static constexpr int RHW = RH * RWW;
+    static constexpr int NWORD = (RHW + 31) / 32;
+    static constexpr int NT = NWY * NWX * 32;
+    static constexpr int NST = 3;  // staging pipeline depth (channel blocks in flight)
+    static constexpr int SMEM = NST * 16 * PLANE * 4;
+};
+
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, bool SPARSE>
+__global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, const float* __restrict__ src,
+                                                                   const float* __restrict__ filt,
+                                                                   float* __restrict__ dst,
+                                                                   unsigned long long* __restrict__ exec_ctr) {
+    using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
+    using AY = typename Gm::AY;
+    using AX = typename Gm::AX;
+    constexpr int RH = Gm::RH, RWW = Gm::RWW, NQ = Gm::NQ, CRH = Gm::CRH, CRW = Gm::CRW, CRWP = Gm::CRWP;
+    constexpr int PLANE = Gm::PLANE, RHW = Gm::RHW, NWORD = Gm::NWORD, NT = Gm::NT;
+    constexpr int TAPS = R * S;
+    static_assert(Gm::XSTEP % 4 == 0 || NWX == 1, "warp regions must stay 16B aligned");
+
+    // channel-major staging of the swept tensor: [buf][16 channels][CRH][CRWP]
+    extern __shared__ __align__(16) float Ds[];
+
+    const int Co = FWD ? sh.K : sh.C, Ci = FWD ? sh.C : sh.K;
+    const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
+    const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
+    const int CiB = Ci / 16, CoB = Co / 16;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wy = warp / NWX, wx = warp % NWX;
+    const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
+    const int ty_idx = blockIdx.x / tiles_x, tx_idx = blockIdx.x % tiles_x;
+    const int yc0 = ty_idx * TH * NWY, xc0 = tx_idx * TW * NWX;  // target origin of the CTA
+    const int y0 = yc0 + wy * TH, x0 = xc0 + wx * TW;              // target origin of this warp
+    const int i = blockIdx.y;
+    const int k0 = blockIdx.z * 32 * KK + lane * KK;  // this lane's channels k0 .. k0+KK-1
+
+    // source origin of the CTA region
+    const int sy0 = FWD ? yc0 * STR - AY::PAD : yc0 / STR + AY::R0;
+    const int sx0 = FWD ? xc0 * STR - AX::PAD : xc0 / STR + AX::R0;
+
+    // filter element (k0, c = 16*cb + cl, u, v) at
+    // (((k/16*CiB + cb)*S + v)*R + u)*256 + cl*16 + k%16
+    const float* fbase = filt + (size_t)(k0 / 16) * CiB * TAPS * 256 + (k0 % 16);
+    const float* sbase = src + (size_t)i * CiB * Hs * Ws * 16;
+
+    // 4-byte cp.async transposes pixel-major global vectors into channel
+    // planes (zero-filled outside the image = virtual padding)
+    auto stage = [&](int cb, int buf) {
+        const float* sp = sbase + (size_t)cb * Hs * Ws * 16;
+        const uint32_t d0 = smem_u32(Ds + buf * 16 * PLANE);
+        for (int idx = threadIdx.x; idx < CRH * CRW * 16; idx += NT) {
+            const int ch = idx & 15, p = idx >> 4;
+            const int ry = p / CRW, rx = p - ry * CRW;
+            const int gy = sy0 + ry, gx = sx0 + rx;
+            const bool ok = gy >= 0 && gy < Hs && gx >= 0 && gx < Ws;
+            const float* g = ok ? sp + ((size_t)gy * Ws + gx) * 16 + ch : sp;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                             d0 + (uint32_t)(ch * PLANE + ry * CRWP + rx) * 4u),
+                         "l"(g), "r"(ok ? 4 : 0));
+        }
+        cp_async_commit();
+    };
+
+    // this warp's region origin inside a channel plane
+    const int woff = wy * Gm::YSTEP * CRWP + wx * Gm::XSTEP;
+
+    // per-lane region pixels q = lane + 32w: plane offset and valid-tap
+    // weight (number of (target, tap) pairs whose target is in the image)
+    int qoff[NWORD];
+    uint32_t wt[NWORD], nzc[NWORD];
+#pragma unroll
+    for (int w = 0; w < NWORD; ++w) {
+        const int q = lane + 32 * w;
+        int ny = 0, nx = 0;
+        qoff[w] = woff;
+        if (q < RHW) {
+            const int ry = q / RWW, rx = q % RWW;
+            qoff[w] = woff + ry * CRWP + rx;
+#pragma unroll
+            for (int v = 0; v < S; ++v) {
+                const int t = AY::target(ry, v);
+                if (t >= 0 && y0 + t < Ho) ++ny;
+            }
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const int t = AX::target(rx, u);
+                if (t >= 0 && x0 + t < Wo) ++nx;
+            }
+        }
+        wt[w] = (uint32_t)(ny * nx);
+        nzc[w] = 0;
+    }
+
+    float acc[TH * TW][KK];
+#pragma unroll
+    for (int t = 0; t < TH * TW; ++t)
+#pragma unroll
+        for (int j = 0; j < KK; ++j) acc[t][j] = 0.0f;
+
+    constexpr int NST = Gm::NST;
+#pragma unroll
+    for (int d = 0; d < NST - 1; ++d) {
+        if (d < CiB) stage(d, d);
+        else cp_async_commit();
+    }
+    for (int cb = 0; cb < CiB; ++cb) {
+        if (cb + NST - 1 < CiB) stage(cb + NST - 1, (cb + NST - 1) % NST);
+        else cp_async_commit();  // keep one group per iteration
+        cp_async_wait<NST - 1>();
+        __syncthreads();
+        const float* fcb = fbase + (size_t)cb * TAPS * 256;
+        FVec<KK> g[TAPS];
+#pragma unroll
+        for (int f = 0; f < TAPS; ++f) g[f].load(fcb + f * 256);
+
+#pragma unroll 1
+        for (int c = 0; c < 16; ++c) {
+            const float* P = Ds + (cb % NST) * 16 * PLANE + c * PLANE;
+            FVec<KK> gn[TAPS];  // next channel's taps, in flight during this channel
+            if (c + 1 < 16) {
+#pragma unroll
+                for (int f = 0; f < TAPS; ++f) gn[f].load(fcb + f * 256 + (c + 1) * 16);
+            }
+            uint32_t m[NWORD];
+            if (SPARSE) {
+#pragma unroll
+                for (int w = 0; w < NWORD; ++w) {
+                    const bool nz = (lane + 32 * w < RHW) && P[qoff[w]] != 0.0f;
+                    nzc[w] += nz ? 1u : 0u;
+                    m[w] = __ballot_sync(0xffffffffu, nz);
+                }
+            }
+            const float* Pw = P + woff;
+            float4 cur[NQ], nxt[NQ];
+#pragma unroll
+            for (int h = 0; h < NQ; ++h) cur[h] = *reinterpret_cast<const float4*>(Pw + 4 * h);
+#pragma unroll
+            for (int ry = 0; ry < RH; ++ry) {
+                if (ry + 1 < RH) {
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h)
+                        nxt[h] = *reinterpret_cast<const float4*>(Pw + (ry + 1) * CRWP + 4 * h);
+                }
+#pragma unroll
+                for (int rx = 0; rx < RWW; ++rx) {
+                    const int p = ry * RWW + rx;
+                    if (!SPARSE || ((m[p >> 5] >> (p & 31)) & 1u)) {
+                        const float4 q4 = cur[rx >> 2];
+                        const float d = (rx & 3) == 0 ? q4.x : (rx & 3) == 1 ? q4.y : (rx & 3) == 2 ? q4.z : q4.w;
+#pragma unroll
+                        for (int v = 0; v < S; ++v) {
+                            const int ty = AY::target(ry, v);
+                            if (ty < 0) continue;
+#pragma unroll
+                            for (int u = 0; u < R; ++u) {
+                                const int tx = AX::target(rx, u);
+                                if (tx < 0) continue;
+#pragma unroll
+                                for (int j = 0; j < KK; ++j)
+                                    acc[ty * TW + tx][j] = fmaf(d, g[v * R + u].v[j], acc[ty * TW + tx][j]);
+                            }
+                        }
+                    }
+                }
+                if (ry + 1 < RH) {
+#pragma unroll
+                    for (int h = 0; h < NQ; ++h) cur[h] = nxt[h];
+                }
+            }
+            if (c + 1 < 16) {
+#pragma unroll
+                for (int f = 0; f < TAPS; ++f) g[f] = gn[f];
+            }
+        }
+        __syncthreads();
+    }
+
+    // epilogue: every valid output written exactly once
+#pragma unroll
+    for (int ty = 0; ty < TH; ++ty) {
+        const int y = y0 + ty;
+        if (y >= Ho) break;
+#pragma unroll
+        for (int tx = 0; tx < TW; ++tx) {
+            const int x = x0 + tx;
+            if (x >= Wo) break;
+            FVec<KK> o;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) o.v[j] = acc[ty * TW + tx][j];
+            o.store(dst + ((((size_t)i * CoB + k0 / 16) * Ho + y) * Wo + x) * 16 + (k0 % 16));
+        }
+    }
+    if (SPARSE && exec_ctr) {
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int w = 0; w < NWORD; ++w) cnt += nzc[w] * wt[w];
+        const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0 && total) atomicAdd(exec_ctr, (unsigned long long)total * (2 * KK));
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR>
+static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
+                              unsigned long long* exec_ctr, cudaStream_t st) {
+    using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
+    const int Co = FWD ? sh.K : sh.C;
+    const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
+    const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
+    const int tiles_y = (Ho + TH * NWY - 1) / (TH * NWY);
+    dim3 grid(tiles_x * tiles_y, sh.N, Co / (32 * KK));
+    auto kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, true>
+                       : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, false>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
+        auto kern2 = !sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, true>
+                             : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, false>;
+        cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
+        attr_set = true;
+    }
+    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr);
+    note_launch();
+    return cudaGetLastError();
+}
+
+bool tile_conv_supported(bool fwd, const DevShape& sh, int V) {
+    if (V != 16) return false;
+    const int Co = fwd ? sh.K : sh.C;
+    if (Co % 64) return false;
+    if (sh.R != sh.S || sh.O != sh.P) return false;
+    if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
+    if (sh.R == 3 && (sh.O == 1 || sh.O == 2)) return true;
+    if (sh.R == 1 && (sh.O == 1 || sh.O == 2)) return true;
+    return false;
+}
+
+#ifndef SPC_CONV_CFG
+#define SPC_CONV_CFG 0
+#endif
+
+cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
+                             float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    const int Co = fwd ? sh.K : sh.C;
+    const bool kk4 = Co % 128 == 0;
+#define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
+    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st)
+    if (sh.R == 3 && sh.O == 1) {
+        if (fwd) {
+            if (kk4) SPC_L(true, 4, 4, 4, 2, 2, 3, 1);
+            SPC_L(true, 2, 4, 8, 2, 1, 3, 1);
+        }
+        if (kk4) SPC_L(false, 4, 4, 4, 2, 2, 3, 1);
+        SPC_L(false, 2, 4, 8, 2, 1, 3, 1);
+    }
+    if (sh.R == 3) {  // stride 2
+        if (fwd) {
+            if (kk4) SPC_L(true, 4, 4, 4, 2, 1, 3, 2);
+            SPC_L(true, 2, 4, 4, 2, 1, 3, 2);
+        }
+        if (kk4) SPC_L(false, 4, 4, 8, 2, 1, 3, 2);
+        SPC_L(false, 2, 4, 8, 2, 1, 3, 2);
+    }
+    if (sh.O == 1) {  // 1x1
+        if (fwd) {
+            if (kk4) SPC_L(true, 4, 4, 8, 2, 1, 1, 1);
+            SPC_L(true, 2, 4, 8, 2, 1, 1, 1);
+        }
+        if (kk4) SPC_L(false, 4, 4, 8, 2, 1, 1, 1);
+        SPC_L(false, 2, 4, 8, 2, 1, 1, 1);
+    }
+    // 1x1 stride 2
+    if (fwd) {
+        if (kk4) SPC_L(true, 4, 4, 8, 2, 1, 1, 2);
+        SPC_L(true, 2, 4, 8, 2, 1, 1, 2);
+    }
+    if (kk4) SPC_L(false, 4, 4, 8, 2, 1, 1, 2);
+    SPC_L(false, 2, 4, 8, 2, 1, 1, 2);
+#undef SPC_L
+}
+
+}  // namespace spc

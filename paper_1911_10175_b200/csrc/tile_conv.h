@@ -1,0 +1,9 @@
+// tile_conv.h -- tuned V=16 FWD/BWI tile kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace spc {
+bool tile_conv_supported(bool fwd, const DevShape& sh, int V);
+cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
+                             float* dst, unsigned long long* exec_ctr, cudaStream_t st);
+}  // namespace spc

@@ -338,3 +338,29 @@ def test_config1_full_size_matches_reference_cpu(sp, comp, check):
         sl = sh.with_batch(2).astuple()
         ref2 = O.dense(comp, sl, a[:2], b)
         assert O.max_abs_rel(got[:2], ref2) <= TOL
+
+
+@pytest.mark.parametrize("R,stride", [(3, 1), (3, 2), (1, 1), (1, 2)])
+def test_tuned_tile_kernels_match_oracle(sp, R, stride):
+    """The V=16 tile kernels (C,K multiples of 64) on ragged image sizes that
+    leave partial tiles, both KK variants, sparse and dense mode, exact counts."""
+    V = 16
+    rng = np.random.default_rng(1000 + 10 * R + stride)
+    cases = [(2, 64, 64, 13, 11), (1, 128, 64, 9, 17), (2, 64, 128, 10, 10), (1, 128, 256, 7, 15),
+             (3, 192, 64, 5, 6)]
+    for n, C, K, H, W in cases:
+        if H + 2 * ((R - 1) // 2) < R:
+            continue
+        sh = sp.ConvShape.make(n, C, K, H, W, R, R, stride, stride)
+        s = float(rng.choice([0.0, 0.5, 0.9]))
+        for comp, check in ALL[:2]:
+            a, b, ba, bb = make_inputs(sp, sh, comp, check, s, V, int(rng.integers(1, 1000)))
+            ref = O.dense(comp, sh.astuple(), a, b)
+            want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), comp, V, 30, check), a)
+            for mode in (0, 1):
+                _, res, got = run(sp, sh, comp, check, V, ba, bb, mode)
+                assert O.max_abs_rel(got, ref) <= TOL, (sh, comp, s, mode)
+                if mode == 0:
+                    assert res.counters.executed_vector_fmas == want["executed_vector_fmas"], (sh, comp, s)
+                else:
+                    assert res.counters.executed_vector_fmas == want["dense_total"]
