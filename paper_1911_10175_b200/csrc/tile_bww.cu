@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
     const int tiles_x = (sh.Wp + TW - 1) / TW;
     const int ntiles = tiles_x * ((sh.Hp + TH - 1) / TH);
     const int nb = (sh.N + 15) / 16;
-    const long items = (long)nb * ntiles;
-    const long it0 = items * blockIdx.z / splits, it1 = items * (blockIdx.z + 1) / splits;
+    const int items = nb * ntiles;
+    const int it0 = (int)((long)items * blockIdx.z / splits), it1 = (int)((long)items * (blockIdx.z + 1) / splits);
 
     float acc[CB][TAPS][KK];
 #pragma unroll
@@ -119,49 +119,79 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
 #pragma unroll
             for (int j = 0; j < KK; ++j) acc[a][f][j] = 0.0f;
 
-    auto origin = [&](long it, int& ib, int& y0, int& x0) {
+    auto origin = [&](int it, int& ib, int& y0, int& x0) {
         ib = (int)(it / ntiles);
         const int t = (int)(it % ntiles);
         y0 = (t / tiles_x) * TH;
         x0 = (t % tiles_x) * TW;
     };
-    auto nimg_of = [&](long it) { return min(16, sh.N - (int)(it / ntiles) * 16); };
+    const int nlast = sh.N - (nb - 1) * 16;  // images in the last (possibly ragged) block
+    auto nimg_of = [&](int it) { return it >= (nb - 1) * ntiles ? nlast : 16; };
 
     // One pipeline stage = one (item, image): the checked planes of that image
     // (4-byte cp.async out of the 16-image CHWNn vectors; .ca keeps the lines in
     // L1 for the item's other images) and the other operand's pixel tile
-    // ([pixel][32*KK lane channels], 16-byte cp.async).
-    auto stage = [&](long it, int j, int buf) {
+    // ([pixel][32*KK lane channels], 16-byte cp.async).  Each thread's element
+    // descriptors (global offset without the image term, smem offset, valid)
+    // are computed once per item.
+    constexpr int NCE = (NCH * CRH * CRW + NWC * 32 - 1) / (NWC * 32);
+    constexpr int NOE = (OTH * OTW * 8 * KK + NWC * 32 - 1) / (NWC * 32);
+    uint32_t cgo[NCE], cso[NCE], ogo[NOE];
+    uint32_t cvalid = 0, ovalid = 0;
+    const size_t ostride_img = (size_t)LcB * Ho * Wo * 16;
+    auto describe = [&](int it) {
         int ib, y0, x0;
         origin(it, ib, y0, x0);
-        float* base = smem + buf * G::STAGE;
-        const uint32_t dc = smem_u32(base);
         const int cy0 = CHECK_INPUT ? y0 * STR - G::PADH : y0;
         const int cx0 = CHECK_INPUT ? x0 * STR - G::PADW : x0;
-        for (int idx = threadIdx.x; idx < NCH * CRH * CRW; idx += NWC * 32) {
-            const int rx = idx % CRW;
-            const int ry = (idx / CRW) % CRH;
-            const int cc = idx / (CRW * CRH);
+        cvalid = 0;
+#pragma unroll
+        for (int e = 0; e < NCE; ++e) {
+            const int idx = threadIdx.x + e * NWC * 32;
+            const int rx = idx % CRW, ry = (idx / CRW) % CRH, cc = idx / (CRW * CRH);
             const int gy = cy0 + ry, gx = cx0 + rx;
-            const bool ok = gy >= 0 && gy < Hc && gx >= 0 && gx < Wc;
-            const float* g = ok ? chk + ((((size_t)ib * Mc + mc0 + cc) * Hc + gy) * Wc + gx) * 16 + j : chk;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
-                             dc + (uint32_t)(cc * PLANE + ry * CRWP + rx) * 4u),
-                         "l"(g), "r"(ok ? 4 : 0));
+            const bool ok = idx < NCH * CRH * CRW && gy >= 0 && gy < Hc && gx >= 0 && gx < Wc;
+            cgo[e] = ok ? (uint32_t)(((((size_t)ib * Mc + mc0 + cc) * Hc + gy) * Wc + gx) * 16) : 0u;
+            cso[e] = (uint32_t)(cc * PLANE + ry * CRWP + rx) * 4u;
+            cvalid |= (ok ? 1u : 0u) << e;
         }
         const int oy0 = CHECK_INPUT ? y0 : y0 * STR - G::PADH;
         const int ox0 = CHECK_INPUT ? x0 : x0 * STR - G::PADW;
-        const int i = ib * 16 + j;
-        const uint32_t doo = smem_u32(base + G::CFLOATS);
-        for (int idx = threadIdx.x; idx < OTH * OTW * 8 * KK; idx += NWC * 32) {
+        ovalid = 0;
+#pragma unroll
+        for (int e = 0; e < NOE; ++e) {
+            const int idx = threadIdx.x + e * NWC * 32;
             const int c4 = idx % (8 * KK), q = idx / (8 * KK);
             const int gy = oy0 + q / OTW, gx = ox0 + q % OTW;
             const int ch = lc0 + c4 * 4;
-            const bool ok = gy >= 0 && gy < Ho && gx >= 0 && gx < Wo;
-            const float* g =
-                ok ? oth + ((((size_t)i * LcB + ch / 16) * Ho + gy) * Wo + gx) * 16 + (ch % 16) : oth;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(doo + (uint32_t)idx * 16u),
-                         "l"(g), "r"(ok ? 16 : 0));
+            const bool ok = idx < OTH * OTW * 8 * KK && gy >= 0 && gy < Ho && gx >= 0 && gx < Wo;
+            ogo[e] = ok ? (uint32_t)((((size_t)(ib * 16) * LcB + ch / 16) * Ho * Wo + (size_t)gy * Wo + gx) * 16 +
+                                     (ch % 16))
+                        : 0u;
+            ovalid |= (ok ? 1u : 0u) << e;
+        }
+    };
+    auto stage = [&](int j, int buf) {
+        float* base = smem + buf * G::STAGE;
+        const uint32_t dc = smem_u32(base);
+#pragma unroll
+        for (int e = 0; e < NCE; ++e) {
+            const int idx = threadIdx.x + e * NWC * 32;
+            if (idx < NCH * CRH * CRW) {
+                const bool ok = (cvalid >> e) & 1u;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dc + cso[e]),
+                             "l"(chk + cgo[e] + (ok ? j : 0)), "r"(ok ? 4 : 0));
+            }
+        }
+        const uint32_t doo = smem_u32(base + G::CFLOATS);
+#pragma unroll
+        for (int e = 0; e < NOE; ++e) {
+            const int idx = threadIdx.x + e * NWC * 32;
+            if (idx < OTH * OTW * 8 * KK) {
+                const bool ok = (ovalid >> e) & 1u;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(doo + (uint32_t)idx * 16u),
+                             "l"(oth + ogo[e] + (ok ? (size_t)j * ostride_img : 0)), "r"(ok ? 16 : 0));
+            }
         }
     };
 
@@ -175,23 +205,25 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
     uint32_t cnt = 0;
 
     // prefetch cursor runs NST-1 stages ahead of the consumer
-    long pit = it0;
+    int pit = it0;
     int pj = 0;
-    auto advance = [&](long& it, int& j) {
-        if (++j >= nimg_of(it)) {
-            j = 0;
-            ++it;
+    if (pit < it1) describe(pit);
+    auto advance = [&]() {
+        if (++pj >= nimg_of(pit)) {
+            pj = 0;
+            if (++pit < it1) describe(pit);
         }
     };
     for (int d = 0; d < G::NST - 1; ++d) {
         if (pit < it1) {
-            stage(pit, pj, d);
-            advance(pit, pj);
+            stage(pj, d);
+            advance();
         }
         cp_async_commit();
     }
-    int ord = 0;
-    for (long it = it0; it < it1; ++it) {
+    int sbuf = G::NST - 1;  // stage buffer the next prefetch fills
+    int cbufi = 0;          // stage buffer the consumer reads
+    for (int it = it0; it < it1; ++it) {
         int ib, y0, x0;
         origin(it, ib, y0, x0);
         const int nimg = nimg_of(it);
@@ -232,16 +264,16 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
         }
 
 #pragma unroll 1
-        for (int j = 0; j < nimg; ++j, ++ord) {
+        for (int j = 0; j < nimg; ++j) {
             if (pit < it1) {
-                stage(pit, pj, (ord + G::NST - 1) % G::NST);
-                advance(pit, pj);
+                stage(pj, sbuf);
+                advance();
             }
             cp_async_commit();
             cp_async_wait<G::NST - 1>();
             __syncthreads();
 
-            const float* base = smem + (ord % G::NST) * G::STAGE;
+            const float* base = smem + cbufi * G::STAGE;
             float O[OTH * OTW][KK];
             const float* Ob = base + G::CFLOATS + lane * KK;
 #pragma unroll
@@ -313,6 +345,8 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
                 }
             }
             __syncthreads();  // stage buffer free for reuse
+            sbuf = sbuf + 1 == G::NST ? 0 : sbuf + 1;
+            cbufi = cbufi + 1 == G::NST ? 0 : cbufi + 1;
         }
     }
     cp_async_wait<0>();
@@ -406,8 +440,8 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
     return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, STR>(sparse, sh, chk, oth, dst, exec_ctr, st)
     if (check_input) {
         if (sh.R == 3 && sh.O == 1) {
-            if (kk4) SPC_B(true, 4, 2, 4, 4, 4, 3, 1);
-            SPC_B(true, 2, 4, 4, 4, 4, 3, 1);
+            if (kk4) SPC_B(true, 4, 1, 8, 4, 4, 3, 1);
+            SPC_B(true, 2, 2, 8, 4, 4, 3, 1);
         }
         if (sh.R == 3) {
             if (kk4) SPC_B(true, 4, 2, 4, 2, 4, 3, 2);
@@ -421,8 +455,8 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
         SPC_B(true, 2, 4, 4, 4, 8, 1, 2);
     }
     if (sh.R == 3 && sh.O == 1) {
-        if (kk4) SPC_B(false, 4, 2, 4, 2, 4, 3, 1);
-        SPC_B(false, 2, 2, 4, 4, 4, 3, 1);
+        if (kk4) SPC_B(false, 4, 1, 8, 2, 4, 3, 1);
+        SPC_B(false, 2, 2, 8, 4, 4, 3, 1);
     }
     if (sh.R == 3) {
         if (kk4) SPC_B(false, 4, 2, 4, 2, 2, 3, 2);

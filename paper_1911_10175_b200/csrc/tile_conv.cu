@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 #pragma unroll 1
         for (int c = 0; c < 16; ++c) {
             const float* P = Ds + (cb % NST) * 16 * PLANE + c * PLANE;
-            FVec<KK> gn[TAPS];  // next channel's taps, in flight during this channel
+            // next channel's filter taps (L1 hits for all but the CTA's first
+            // warp), in flight while this channel computes
+            FVec<KK> gn[TAPS];
             if (c + 1 < 16) {
 #pragma unroll
                 for (int f = 0; f < TAPS; ++f) gn[f].load(fcb + f * 256 + (c + 1) * 16);
