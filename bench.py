@@ -325,11 +325,14 @@ def main():
     useful = sum(2.0 * V * exec_fmas[(work[i][0], work[i][1], dom)] for i in dom_idx)
     dom_ms = sum(per_launch_ms[i] for i in dom_idx)
     achieved = useful / (dom_ms * 1e-3) / 1e12
-    traffic = load_traffic(dom)
+    traffic, traffic_src = load_traffic(dom)
     roofline = {"bound": "fp32", "kernel": f"{dom} tile kernel ({len(dom_idx)} launches/step)",
                 "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4) if peak else None,
                 "traffic": traffic,
+                "traffic_note": (f"dram__bytes_read+write per launch, {traffic_src['launch']}, "
+                                 f"{traffic_src['traffic_over_algorithmic']}x its algorithmic bytes "
+                                 f"({traffic_src['source']})") if traffic_src else None,
                 "basis": "useful FLOPs = 2*V*executed_vector_fmas (exact in-kernel count) per launch / "
                          "CUDA-event launch duration; peak = live FFMA-pipe probe (MEASURED_PEAKS.json has no "
                          "FP32 entry)",
@@ -381,10 +384,10 @@ def load_traffic(family):
     """dram bytes per launch of the dominant kernel, from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get(family)
+        d = json.load(open(p))[family]
+        return d["dram_bytes_per_launch"], d
     except Exception:
-        return None
+        return None, None
 
 
 def dense_baseline(sp, wl, layers, dev, sptr, V):

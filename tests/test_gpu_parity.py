@@ -364,3 +364,16 @@ def test_tuned_tile_kernels_match_oracle(sp, R, stride):
                     assert res.counters.executed_vector_fmas == want["executed_vector_fmas"], (sh, comp, s)
                 else:
                     assert res.counters.executed_vector_fmas == want["dense_total"]
+
+
+def test_cxx_dropin_matches_reference_library():
+    """The C++ drop-in (spconv::cuda::*) against the reference's own
+    spconv::run_parallel on identical blocked tensors (tests/cxx/test_dropin.cpp)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_1911_10175_b200", "cxx", "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("C++ drop-in test binary not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:]
