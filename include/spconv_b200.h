@@ -156,6 +156,11 @@ uint64_t spc_launch_count(void);
  * thread running `iters` x 16 independent FFMAs; out[0] receives a checksum.
  * Returns the kernel's FLOP count in *flops (time it with events). */
 spc_status spc_ffma_peak_kernel(float* out, int blocks, int iters, double* flops, void* stream);
+/* Development: run FWD/BWI with tile-kernel variant `variant` (3x3 stride 1,
+ * V=16 only; see launch_tile_conv_variant).  Same validation as spc_sparse_*. */
+spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
+                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
+                                  void* stream);
 /* Write `n` floats of scratch (an L2 flush between timed steps). */
 spc_status spc_l2_flush(float* scratch, size_t n, void* stream);
 

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "dispatch.h"
+#include "tile_conv.h"
 
 namespace spc {
 
@@ -617,6 +618,22 @@ spc_status spc_ffma_peak_kernel(float* out, int blocks, int iters, double* flops
     if (flops) *flops = 2.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SPC_OK : cuda_fail(e, "ffma peak");
+}
+
+spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
+                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
+                                  void* stream) {
+    if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    const bool fwd = plan->comp == SPC_FWD;
+    spc_status s = fwd ? validate_fwd(src, filt, *shape, *plan) : validate_bwi(src, filt, *shape, *plan);
+    if (s) return s;
+    if ((s = prepare_dst(*shape, *plan, dst))) return s;
+    if ((s = check_device())) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = start_counters(*shape, *plan, mode, d_counters, st))) return s;
+    cudaError_t e = launch_tile_conv_variant(variant, fwd, mode == SPC_SPARSE, make_dev_shape(*shape), src->data,
+                                             filt->data, dst->data, exec_slot(d_counters, mode), st);
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "variant launch");
 }
 
 spc_status spc_l2_flush(float* scratch, size_t n, void* stream) {

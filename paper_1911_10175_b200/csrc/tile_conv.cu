@@ -24,6 +24,7 @@
 // that pixel) per channel block; the warp total x (2*KK vectors) is the
 // reference's count (P/src/kernel_impl.hpp:188-189) independent of tiling.
 #include "common.cuh"
+#include "jt_blocks.cuh"
 #include "tile_conv.h"
 
 namespace spc {
@@ -63,6 +64,21 @@ struct FVec<4> {
     }
     __device__ __forceinline__ void store(float* p) const {
         *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+
+template <>
+struct FVec<8> {
+    float v[8];
+    __device__ __forceinline__ void load(const float* p) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        const float4 u = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+        v[4] = u.x; v[5] = u.y; v[6] = u.z; v[7] = u.w;
+    }
+    __device__ __forceinline__ void store(float* p) const {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        *(reinterpret_cast<float4*>(p) + 1) = make_float4(v[4], v[5], v[6], v[7]);
     }
 };
 
@@ -109,12 +125,34 @@ struct ConvGeom {
     static constexpr int SMEM = NST * 16 * PLANE * 4;
 };
 
-template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, bool SPARSE>
+// Static loop over the 32-pixel mask words of the jump-table path.
+template <int W, int NW, class JB, class Acc, class Gv>
+__device__ __forceinline__ void jt_words(Acc& acc, const Gv& g, const float* vv, const uint32_t* m) {
+    if constexpr (W < NW) {
+        if (m[W]) JB::template Word<W>::run(acc, g, vv[W], m[W]);
+        jt_words<W + 1, NW, JB>(acc, g, vv, m);
+    }
+}
+
+// GPF selects how the next channel's filter taps are fetched: 0 = L1
+// prefetch + just-in-time loads (fewer registers), 1 = register double
+// buffer (latency fully hidden, +R*S*KK registers).
+// JT selects the sparse inner loop: 0 = one uniform branch per region pixel;
+// 100 = jump-table dispatch over the nonzero pixels only (jt_blocks.cuh,
+// generated); 1..99 = a CTA-collective choice per 16-channel block: the jump
+// table when the previous block's measured density (nonzeros / region
+// pixels, summed over the CTA's warps) is at most JT%, else per-pixel
+// branches.  All variants accumulate in the same order (bitwise identical).
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF, int JT, bool SPARSE>
 __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, const float* __restrict__ src,
                                                                    const float* __restrict__ filt,
                                                                    float* __restrict__ dst,
-                                                                   unsigned long long* __restrict__ exec_ctr) {
+                                                                   unsigned long long* __restrict__ exec_ctr,
+                                                                   const int* __restrict__ sel, int want) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
+    // device-side kernel choice (see launch_tile_conv): the variant whose
+    // selector value does not match exits before touching memory
+    if (sel != nullptr && __ldg(sel) != want) return;
     using AY = typename Gm::AY;
     using AX = typename Gm::AX;
     constexpr int RH = Gm::RH, RWW = Gm::RWW, NQ = Gm::NQ, CRH = Gm::CRH, CRW = Gm::CRW, CRWP = Gm::CRWP;
@@ -124,6 +162,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 
     // channel-major staging of the swept tensor: [buf][16 channels][CRH][CRWP]
     extern __shared__ __align__(16) float Ds[];
+    __shared__ int wnnz[NWY * NWX];  // per-warp nonzero count of the last channel block
 
     const int Co = FWD ? sh.K : sh.C, Ci = FWD ? sh.C : sh.K;
     const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
@@ -133,11 +172,15 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wy = warp / NWX, wx = warp % NWX;
     const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
-    const int ty_idx = blockIdx.x / tiles_x, tx_idx = blockIdx.x % tiles_x;
+    // blockIdx.x = tile * groups + channel group: the CTAs that share a source
+    // region run back to back, so the second read of it hits L2
+    const int ngroups = Co / (32 * KK);
+    const int kg = blockIdx.x % ngroups, tile = blockIdx.x / ngroups;
+    const int ty_idx = tile / tiles_x, tx_idx = tile % tiles_x;
     const int yc0 = ty_idx * TH * NWY, xc0 = tx_idx * TW * NWX;  // target origin of the CTA
     const int y0 = yc0 + wy * TH, x0 = xc0 + wx * TW;              // target origin of this warp
     const int i = blockIdx.y;
-    const int k0 = blockIdx.z * 32 * KK + lane * KK;  // this lane's channels k0 .. k0+KK-1
+    const int k0 = kg * 32 * KK + lane * KK;  // this lane's channels k0 .. k0+KK-1
 
     // source origin of the CTA region
     const int sy0 = FWD ? yc0 * STR - AY::PAD : yc0 / STR + AY::R0;
@@ -203,6 +246,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         for (int j = 0; j < KK; ++j) acc[t][j] = 0.0f;
 
     constexpr int NST = Gm::NST;
+    bool use_jt = JT >= 100;  // JT in 1..99: decided per block below, starting with branches
 #pragma unroll
     for (int d = 0; d < NST - 1; ++d) {
         if (d < CiB) stage(d, d);
@@ -214,29 +258,52 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         cp_async_wait<NST - 1>();
         __syncthreads();
         const float* fcb = fbase + (size_t)cb * TAPS * 256;
+        int blk_nnz = 0;  // this warp's region nonzeros over the block (uniform)
         FVec<KK> g[TAPS];
+        if constexpr (GPF == 1) {
 #pragma unroll
-        for (int f = 0; f < TAPS; ++f) g[f].load(fcb + f * 256);
+            for (int f = 0; f < TAPS; ++f) g[f].load(fcb + f * 256);
+        }
 
 #pragma unroll 1
         for (int c = 0; c < 16; ++c) {
             const float* P = Ds + (cb % NST) * 16 * PLANE + c * PLANE;
-            // next channel's filter taps (L1 hits for all but the CTA's first
-            // warp), in flight while this channel computes
-            FVec<KK> gn[TAPS];
-            if (c + 1 < 16) {
+            FVec<KK> gn[GPF == 1 ? TAPS : 1];
+            if constexpr (GPF == 0) {
+                // this channel's taps: L1 hits (prefetched one channel ahead,
+                // shared by the CTA's warps), issued before the mask ballots so
+                // the two latencies overlap
+#pragma unroll
+                for (int f = 0; f < TAPS; ++f) g[f].load(fcb + f * 256 + c * 16);
+                const float* nf = c + 1 < 16 ? fcb + (c + 1) * 16 : fcb + TAPS * 256;
+                if (cb + 1 < CiB || c + 1 < 16) {
+#pragma unroll
+                    for (int f = 0; f < TAPS; ++f) asm volatile("prefetch.global.L1 [%0];" ::"l"(nf + f * 256));
+                }
+            } else if (c + 1 < 16) {
+                // next channel's taps in flight while this channel computes
 #pragma unroll
                 for (int f = 0; f < TAPS; ++f) gn[f].load(fcb + f * 256 + (c + 1) * 16);
             }
             uint32_t m[NWORD];
+            float vv[NWORD];
             if (SPARSE) {
 #pragma unroll
                 for (int w = 0; w < NWORD; ++w) {
-                    const bool nz = (lane + 32 * w < RHW) && P[qoff[w]] != 0.0f;
+                    vv[w] = (lane + 32 * w < RHW) ? P[qoff[w]] : 0.0f;
+                    const bool nz = vv[w] != 0.0f;
                     nzc[w] += nz ? 1u : 0u;
                     m[w] = __ballot_sync(0xffffffffu, nz);
                 }
             }
+            using JB = JtBlocks<FWD, KK, TH, TW, R, S, STR>;
+            if constexpr (SPARSE && JT > 0 && JT < 100) {
+#pragma unroll
+                for (int w = 0; w < NWORD; ++w) blk_nnz += __popc(m[w]);
+            }
+            if (use_jt) {
+                if constexpr (SPARSE && JT > 0 && JB::available) jt_words<0, NWORD, JB>(acc, g, vv, m);
+            } else {
             const float* Pw = P + woff;
             float4 cur[NQ], nxt[NQ];
 #pragma unroll
@@ -274,12 +341,24 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                     for (int h = 0; h < NQ; ++h) cur[h] = nxt[h];
                 }
             }
-            if (c + 1 < 16) {
+            }  // in-line path
+            if constexpr (GPF == 1) {
+                if (c + 1 < 16) {
 #pragma unroll
-                for (int f = 0; f < TAPS; ++f) g[f] = gn[f];
+                    for (int f = 0; f < TAPS; ++f) g[f] = gn[f];
+                }
             }
         }
+        if constexpr (SPARSE && JT > 0 && JT < 100) {
+            if (lane == 0) wnnz[warp] = blk_nnz;
+        }
         __syncthreads();
+        if constexpr (SPARSE && JT > 0 && JT < 100) {
+            int tot = 0;
+#pragma unroll
+            for (int w = 0; w < NWY * NWX; ++w) tot += wnnz[w];
+            use_jt = (long)tot * 100 <= (long)JT * 16 * NWY * NWX * RHW;
+        }
     }
 
     // epilogue: every valid output written exactly once
@@ -307,28 +386,110 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 }
 
 // ---------------------------------------------------------------- dispatch
-template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR>
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF = 1, int JT = 0>
 static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
-                              unsigned long long* exec_ctr, cudaStream_t st) {
+                              unsigned long long* exec_ctr, cudaStream_t st, const int* sel = nullptr,
+                              int want = 0) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     const int Co = FWD ? sh.K : sh.C;
     const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
     const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
     const int tiles_y = (Ho + TH * NWY - 1) / (TH * NWY);
-    dim3 grid(tiles_x * tiles_y, sh.N, Co / (32 * KK));
-    auto kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, true>
-                       : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, false>;
+    dim3 grid(tiles_x * tiles_y * (Co / (32 * KK)), sh.N, 1);
+    auto kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true>
+                       : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
-        auto kern2 = !sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, true>
-                             : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, false>;
+        auto kern2 = !sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true>
+                             : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false>;
         cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
         attr_set = true;
     }
-    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr);
+    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want);
     note_launch();
     return cudaGetLastError();
+}
+
+// Development entry: time alternative tile configurations of the 3x3 s1
+// kernel (tools/tune.py).  Returns cudaErrorInvalidValue for an unknown or
+// inapplicable variant.
+cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const DevShape& sh, const float* src,
+                                     const float* filt, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    const int Co = fwd ? sh.K : sh.C;
+    if (sh.R != 3 || sh.O != 1) return cudaErrorInvalidValue;
+#define SPC_V(ID, KK, TH, TW, NWY, NWX, GPF) SPC_VJ(ID, KK, TH, TW, NWY, NWX, GPF, 0)
+#define SPC_VJ(ID, KK, TH, TW, NWY, NWX, GPF, JT)                                                               \
+    case ID:                                                                                                    \
+        if (Co % (32 * KK)) return cudaErrorInvalidValue;                                                       \
+        return fwd ? launch_cfg<true, KK, TH, TW, NWY, NWX, 3, 3, 1, GPF, JT>(sparse, sh, src, filt, dst, exec_ctr, st) \
+                   : launch_cfg<false, KK, TH, TW, NWY, NWX, 3, 3, 1, GPF, JT>(sparse, sh, src, filt, dst, exec_ctr, st);
+    switch (variant) {
+        SPC_V(0, 4, 4, 4, 2, 2, 1)
+        SPC_V(1, 4, 4, 4, 2, 2, 0)
+        SPC_V(2, 4, 4, 8, 2, 1, 1)
+        SPC_V(3, 4, 4, 8, 2, 1, 0)
+        SPC_V(4, 4, 8, 4, 2, 1, 0)
+        SPC_V(5, 2, 8, 8, 2, 1, 0)
+        SPC_V(6, 2, 4, 8, 2, 2, 1)
+        SPC_V(7, 8, 4, 4, 2, 1, 0)
+        SPC_V(8, 8, 2, 4, 2, 2, 0)
+        SPC_V(9, 8, 2, 4, 2, 2, 1)
+        SPC_V(10, 4, 4, 4, 4, 1, 1)
+        SPC_V(11, 4, 4, 4, 1, 4, 1)
+        SPC_V(12, 2, 4, 8, 4, 1, 1)
+        SPC_V(13, 4, 2, 8, 4, 1, 1)
+        SPC_VJ(14, 2, 4, 8, 2, 2, 1, 100)
+        SPC_VJ(15, 2, 4, 8, 4, 1, 1, 100)
+        SPC_VJ(16, 4, 4, 4, 2, 2, 1, 100)
+        SPC_VJ(17, 4, 4, 8, 2, 1, 1, 100)
+        SPC_VJ(18, 4, 4, 8, 2, 1, 0, 100)
+        SPC_VJ(19, 2, 4, 8, 2, 2, 0, 100)
+        SPC_VJ(20, 2, 4, 8, 2, 2, 1, 15)
+        SPC_VJ(21, 4, 4, 4, 2, 2, 1, 15)
+        SPC_VJ(22, 4, 4, 8, 2, 1, 1, 15)
+        SPC_VJ(23, 4, 4, 4, 2, 2, 1, 30)
+        SPC_VJ(24, 4, 4, 8, 2, 1, 1, 30)
+        SPC_VJ(25, 2, 4, 8, 2, 2, 1, 30)
+        default: return cudaErrorInvalidValue;
+    }
+#undef SPC_V
+#undef SPC_VJ
+}
+
+// Nonzero density of the swept tensor from a strided sample (i.i.d. or
+// spatially correlated data alike: 148*256 threads x 16 float4 spread over
+// the whole tensor).  sel = 1 when density <= pct% (the jump-table kernel
+// wins), else 0.
+__global__ void __launch_bounds__(256) density_probe_kernel(const float* __restrict__ t, size_t n, int pct,
+                                                            int* __restrict__ sel) {
+    __shared__ unsigned long long cnt[2];
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const size_t n4 = n / 4;
+    const size_t nthreads = (size_t)gridDim.x * blockDim.x;
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t stride = n4 / (nthreads * 16) > 0 ? n4 / (nthreads * 16) : 1;
+    unsigned nz = 0, tot = 0;
+    for (int i = 0; i < 16; ++i) {
+        const size_t e = (tid + (size_t)i * nthreads) * stride;
+        if (e < n4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(t) + e);
+            nz += (v.x != 0.0f) + (v.y != 0.0f) + (v.z != 0.0f) + (v.w != 0.0f);
+            tot += 4;
+        }
+    }
+    nz = __reduce_add_sync(0xffffffffu, nz);
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&cnt[0], (unsigned long long)nz);
+        atomicAdd(&cnt[1], (unsigned long long)tot);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // one CTA's sample decides for the whole launch when gridDim.x == 1
+        sel[blockIdx.x] = cnt[0] * 100 <= (unsigned long long)pct * cnt[1] ? 1 : 0;
+    }
 }
 
 bool tile_conv_supported(bool fwd, const DevShape& sh, int V) {
@@ -353,12 +514,34 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
 #define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
     return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st)
     if (sh.R == 3 && sh.O == 1) {
-        if (fwd) {
-            if (kk4) SPC_L(true, 4, 4, 4, 2, 2, 3, 1);
-            SPC_L(true, 2, 4, 8, 2, 1, 3, 1);
+        const int Ho = fwd ? sh.Hp : sh.H;
+        if (sparse && kk4) {
+            // both kernels launch; the density probe's selector lets one run
+            const int Ci = fwd ? sh.C : sh.K;
+            const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
+            int* sel = nullptr;
+            cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
+            if (e != cudaSuccess) return e;
+            density_probe_kernel<<<1, 256, 0, st>>>(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel);
+            note_launch();
+            if (Ho <= 28)
+                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
+                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
+            else
+                e = fwd ? launch_cfg<true, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
+                        : launch_cfg<false, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
+            if (e == cudaSuccess)
+                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1)
+                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1);
+            cudaFreeAsync(sel, st);
+            return e;
         }
-        if (kk4) SPC_L(false, 4, 4, 4, 2, 2, 3, 1);
-        SPC_L(false, 2, 4, 8, 2, 1, 3, 1);
+        if (kk4 && !sparse) {
+            if (fwd) SPC_L(true, 4, 4, 8, 2, 1, 3, 1);
+            SPC_L(false, 4, 4, 8, 2, 1, 3, 1);
+        }
+        if (fwd) SPC_L(true, 2, 4, 8, 2, 2, 3, 1);
+        SPC_L(false, 2, 4, 8, 2, 2, 3, 1);
     }
     if (sh.R == 3) {  // stride 2
         if (fwd) {

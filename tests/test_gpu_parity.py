@@ -352,8 +352,8 @@ def test_tuned_tile_kernels_match_oracle(sp, R, stride):
         if H + 2 * ((R - 1) // 2) < R:
             continue
         sh = sp.ConvShape.make(n, C, K, H, W, R, R, stride, stride)
-        s = float(rng.choice([0.0, 0.5, 0.9]))
         for comp, check in ALL[:2]:
+          for s in (0.0, 0.5, 0.93):  # 0.93: the jump-table kernel (density <= 15%) for 128-multiple channels
             a, b, ba, bb = make_inputs(sp, sh, comp, check, s, V, int(rng.integers(1, 1000)))
             ref = O.dense(comp, sh.astuple(), a, b)
             want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), comp, V, 30, check), a)
@@ -364,6 +364,35 @@ def test_tuned_tile_kernels_match_oracle(sp, R, stride):
                     assert res.counters.executed_vector_fmas == want["executed_vector_fmas"], (sh, comp, s)
                 else:
                     assert res.counters.executed_vector_fmas == want["dense_total"]
+
+
+def test_jump_table_and_branch_kernels_agree_bitwise(sp):
+    """The two sparse inner loops (per-pixel branches / jump table over the
+    nonzeros) accumulate in the same order: identical bits, identical counts."""
+    import ctypes as C
+    import torch
+    V = 16
+    L = sp._lib.load()
+    sh = sp.ConvShape.make(2, 128, 128, 20, 22, 3, 3, 1, 1)
+    for comp in (0, 1):
+        for s in (0.5, 0.95):
+            a, b, ba, bb = make_inputs(sp, sh, comp, 0, s, V, 77)
+            pl = sp.plan(sh, sp.Component(comp), V)
+            outs = []
+            for variant in (2, 17):  # same tile (KK=4, 4x8), branches vs jump table
+                out = torch.empty(sh.N * (sh.K if comp == 0 else sh.C) * (sh.out_h() if comp == 0 else sh.H)
+                                  * (sh.out_w() if comp == 0 else sh.W), device="cuda")
+                cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+                ca, cb, cs, cp = ba.to_c(), bb.to_c(), sh.to_c(), pl.to_c()
+                cd = sp._lib.spc_tensor(0, 0, 0, 0, 0, 0, 0, 0, 0, out.data_ptr(), out.numel())
+                st = L.spc_debug_conv_variant(variant, C.byref(ca), C.byref(cb), C.byref(cs), C.byref(cp), 0,
+                                              C.byref(cd), C.c_void_p(cnt.data_ptr()),
+                                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+                assert st == 0, sp._lib.last_error()
+                torch.cuda.synchronize()
+                outs.append((out.cpu().numpy(), cnt.cpu().numpy()))
+            assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+            assert np.array_equal(outs[0][1], outs[1][1])
 
 
 def test_cxx_dropin_matches_reference_library():
