@@ -29,6 +29,7 @@
 // side, i.e. the reference's check=output_grad transpose (kernels.cpp:285-300)
 // is fused into the reduction.
 #include "common.cuh"
+#include "jt_blocks.cuh"
 #include "tile_bww.h"
 
 namespace spc {
@@ -83,12 +84,26 @@ struct BwwGeom {
     static constexpr int SMEM = NST * STAGE * 4;
 };
 
-template <bool CHECK_INPUT, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, bool SPARSE>
+// Static loop over the 32-pixel mask words of the jump-table path.
+template <int W, int NW, class JB, class Acc, class Ov>
+__device__ __forceinline__ void bww_jt_words(Acc& acc, const Ov& O, const float* vv, const uint32_t* m) {
+    if constexpr (W < NW) {
+        if (m[W]) JB::template Word<W>::run(acc, O, vv[W], m[W]);
+        bww_jt_words<W + 1, NW, JB>(acc, O, vv, m);
+    }
+}
+
+// JT = 100: jump-table dispatch over the nonzero checked pixels only
+// (jt_blocks.cuh, generated); 0: one uniform branch per checked pixel.  Same
+// accumulation order either way.  `sel`/`want`: device-side kernel choice.
+template <bool CHECK_INPUT, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, int JT, bool SPARSE>
 __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const float* __restrict__ chk,
                                                             const float* __restrict__ oth,
                                                             float* __restrict__ partial, int splits,
-                                                            unsigned long long* __restrict__ exec_ctr) {
+                                                            unsigned long long* __restrict__ exec_ctr,
+                                                            const int* __restrict__ sel, int want) {
     using G = BwwGeom<CHECK_INPUT, KK, CB, NWC, TH, TW, R, S, STR>;
+    if (sel != nullptr && __ldg(sel) != want) return;
     constexpr int TAPS = G::TAPS, CRH = G::CRH, CRW = G::CRW, CRWP = G::CRWP, PLANE = G::PLANE;
     constexpr int CHW = G::CHW, NWORD = G::NWORD, NQ = G::NQ, OTH = G::OTH, OTW = G::OTW, NCH = G::NCH;
 
@@ -292,14 +307,20 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
             for (int cc = 0; cc < CB; ++cc) {
                 const float* Pl = base + (warp * CB + cc) * PLANE;
                 uint32_t m[NWORD];
+                float vv[NWORD];
                 if (SPARSE) {
 #pragma unroll
                     for (int w = 0; w < NWORD; ++w) {
-                        const bool nz = (lane + 32 * w < CHW) && Pl[qoff[w]] != 0.0f;
+                        vv[w] = (lane + 32 * w < CHW) ? Pl[qoff[w]] : 0.0f;
+                        const bool nz = vv[w] != 0.0f;
                         cnt += nz ? wt[w] : 0u;
                         m[w] = __ballot_sync(0xffffffffu, nz);
                     }
                 }
+                using JB = BwwJtBlocks<CHECK_INPUT, KK, TH, TW, R, S, STR>;
+                if constexpr (SPARSE && JT == 100 && JB::available) {
+                    bww_jt_words<0, NWORD, JB>(acc[cc], O, vv, m);
+                } else {
                 float4 cur[NQ], nxt[NQ];
 #pragma unroll
                 for (int h = 0; h < NQ; ++h) cur[h] = *reinterpret_cast<const float4*>(Pl + 4 * h);
@@ -343,6 +364,7 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
                         for (int h = 0; h < NQ; ++h) cur[h] = nxt[h];
                     }
                 }
+                }  // in-line path
             }
             __syncthreads();  // stage buffer free for reuse
             sbuf = sbuf + 1 == G::NST ? 0 : sbuf + 1;
@@ -390,7 +412,11 @@ __global__ void bww_tile_reduce(DevShape sh, const float* __restrict__ partial, 
 }
 
 // ---------------------------------------------------------------- dispatch
-template <bool CI, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR>
+// Launch kernel variant(s) then the fixed-order split reduction.  With
+// JTSEL, sparse mode launches both the per-pixel-branch kernel and the
+// jump-table kernel; a density probe on the checked tensor picks one on the
+// device (the other exits at entry), no host synchronisation.
+template <bool CI, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, bool JTSEL = false>
 static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* chk, const float* oth,
                                   float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
     using G = BwwGeom<CI, KK, CB, NWC, TH, TW, R, S, STR>;
@@ -405,11 +431,27 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
     cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)splits * E * sizeof(float), st);
     if (e != cudaSuccess) return e;
     dim3 grid(Mc / G::NCH, Lc / (32 * KK), (unsigned)splits);
-    auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, true>
-                       : bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    kern<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr);
-    note_launch();
+    if (sparse && JTSEL) {
+        int* sel = nullptr;
+        e = cudaMallocAsync((void**)&sel, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        const size_t n = (size_t)((sh.N + 15) / 16) * Mc * (CI ? sh.H * sh.W : sh.Hp * sh.Wp) * 16;
+        launch_density_probe(chk, n, 15, sel, st);
+        auto k0 = bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, true>;
+        auto k1 = bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 100, true>;
+        cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        k0<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, sel, 0);
+        k1<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, sel, 1);
+        note_launch(2);
+        cudaFreeAsync(sel, st);
+    } else {
+        auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, true>
+                           : bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        kern<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, nullptr, 0);
+        note_launch();
+    }
     e = cudaGetLastError();
     if (e == cudaSuccess) {
         unsigned rb = (unsigned)((E + 255) / 256);
@@ -440,6 +482,8 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
     return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, STR>(sparse, sh, chk, oth, dst, exec_ctr, st)
     if (check_input) {
         if (sh.R == 3 && sh.O == 1) {
+            // the jump-table BWW variant (JTSEL) measured slower than per-pixel
+            // branches at every sparsity of the VGG sweep; branches only
             if (kk4) SPC_B(true, 4, 1, 8, 4, 4, 3, 1);
             SPC_B(true, 2, 2, 8, 4, 4, 3, 1);
         }

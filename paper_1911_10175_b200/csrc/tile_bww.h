@@ -1,6 +1,7 @@
 // tile_bww.h -- tuned V=16 BWW tile kernels (internal).
 #pragma once
 #include "common.cuh"
+#include "tile_conv.h"
 
 namespace spc {
 bool tile_bww_supported(bool check_input, const DevShape& sh, int V);

@@ -23,6 +23,8 @@
 // adds popcount(its pixel's 16-channel nonzero mask) x (valid output taps of
 // that pixel) per channel block; the warp total x (2*KK vectors) is the
 // reference's count (P/src/kernel_impl.hpp:188-189) independent of tiling.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "jt_blocks.cuh"
 #include "tile_conv.h"
@@ -492,6 +494,14 @@ __global__ void __launch_bounds__(256) density_probe_kernel(const float* __restr
     }
 }
 
+void launch_density_probe(const float* t, size_t n, int pct, int* sel, cudaStream_t st) {
+    // SPC_JT_PCT overrides the jump-table density threshold (0 = never, 100 = always)
+    static const int override_pct = std::getenv("SPC_JT_PCT") ? std::atoi(std::getenv("SPC_JT_PCT")) : -1;
+    if (override_pct >= 0) pct = override_pct;
+    density_probe_kernel<<<1, 256, 0, st>>>(t, n, pct, sel);
+    note_launch();
+}
+
 bool tile_conv_supported(bool fwd, const DevShape& sh, int V) {
     if (V != 16) return false;
     const int Co = fwd ? sh.K : sh.C;
@@ -522,8 +532,7 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             int* sel = nullptr;
             cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
             if (e != cudaSuccess) return e;
-            density_probe_kernel<<<1, 256, 0, st>>>(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel);
-            note_launch();
+            launch_density_probe(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel, st);
             if (Ho <= 28)
                 e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
                         : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);

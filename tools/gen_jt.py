@@ -23,6 +23,12 @@ import os
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_1911_10175_b200", "csrc", "jt_blocks.cuh")
 
+# BWW: (CHECK_INPUT, KK, TH, TW, R, S, STR) -- per (checked channel, word)
+BWW_CONFIGS = [
+    (True, 4, 4, 4, 3, 3, 1), (True, 2, 4, 4, 3, 3, 1),
+    (False, 4, 2, 4, 3, 3, 1), (False, 2, 4, 4, 3, 3, 1),
+]
+
 # (FWD, KK, TH, TW, R, S, STR)
 CONFIGS = [
     (True, 2, 4, 8, 3, 3, 1), (False, 2, 4, 8, 3, 3, 1),
@@ -100,6 +106,54 @@ def word_asm(cfg, w):
     return f'    asm volatile("{body}"\n                 : {outs}\n                 : {ins});'
 
 
+def bww_word_asm(cfg, w):
+    """acc[tap][j] += d * O[q][j] for every (tap, other-tile pixel q) a checked
+    pixel feeds (tile_bww.cu's in-line loop, restated as static lists)."""
+    ci, KK, TH, TW, R, S, STR = cfg
+    irh, irw = (TH - 1) * STR + S, (TW - 1) * STR + R
+    crh, crw = (irh, irw) if ci else (TH, TW)
+    otw = TW if ci else irw
+    chw = crh * crw
+    TAPS = R * S
+    NACC = TAPS * KK
+    NO = (TH * TW if ci else irh * irw)
+    oi = lambda q, j: NACC + q * KK + j
+    V = NACC + NO * KK
+    M = V + 1
+    lines = ["{", ".reg .b32 jm, jt, jp, jn;", ".reg .f32 jd, jdn;", f"mov.b32 jm, %{M};",
+             "brev.b32 jt, jm;", "clz.b32 jp, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
+             f"shfl.sync.idx.b32 jd, %{V}, jp, 31, -1;",
+             "Ljt: .branchtargets " + ", ".join(f"Lb{i}" for i in range(32)) + ", Lend;",
+             "brx.idx.uni jp, Ljt;"]
+    for i in range(32):
+        p = 32 * w + i
+        lines.append(f"Lb{i}:")
+        if p >= chw:
+            lines.append("bra.uni Lend;")
+            continue
+        ry, rx = divmod(p, crw)
+        lines += ["brev.b32 jt, jm;", "clz.b32 jn, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
+                  f"shfl.sync.idx.b32 jdn, %{V}, jn, 31, -1;"]
+        for v in range(S):
+            for u in range(R):
+                if ci:
+                    ny, nx = ry - v, rx - u
+                    if ny < 0 or nx < 0 or ny % STR or nx % STR or ny // STR >= TH or nx // STR >= TW:
+                        continue
+                    q = (ny // STR) * otw + nx // STR
+                else:
+                    q = (ry * STR + v) * otw + rx * STR + u
+                for j in range(KK):
+                    a = (v * R + u) * KK + j
+                    lines.append(f"fma.rn.f32 %{a}, jd, %{oi(q, j)}, %{a};")
+        lines += ["mov.f32 jd, jdn;", "brx.idx.uni jn, Ljt;"]
+    lines += ["Lend:", "}"]
+    body = "\\n\\t".join(lines)
+    outs = ", ".join(f'"+f"(acc[{f}][{j}])' for f in range(TAPS) for j in range(KK))
+    ins = ", ".join(f'"f"(O[{q}][{j}])' for q in range(NO) for j in range(KK)) + ', "f"(v), "r"(m)'
+    return f'        asm volatile("{body}"\n                     : {outs}\n                     : {ins});'
+
+
 def main():
     out = ["// GENERATED by tools/gen_jt.py -- do not edit.",
            "// Jump-table (brx.idx) FMA blocks for tile_conv_kernel's sparse mode; see the",
@@ -129,6 +183,27 @@ def main():
                     "    template <class Acc, class Gv>",
                     "    static __device__ __forceinline__ void run(Acc& acc, const Gv& g, float v, unsigned m) {",
                     word_asm(cfg, w), "    }", "};", ""]
+    out += ["template <bool CI, int KK, int TH, int TW, int R, int S, int STR>",
+            "struct BwwJtBlocks {",
+            "    static constexpr bool available = false;",
+            "    template <int W>",
+            "    struct Word {",
+            "        template <class Acc, class Ov>",
+            "        static __device__ __forceinline__ void run(Acc&, const Ov&, float, unsigned) {}",
+            "    };",
+            "};", ""]
+    for cfg in BWW_CONFIGS:
+        ci, KK, TH, TW, R, S, STR = cfg
+        irh, irw = (TH - 1) * STR + S, (TW - 1) * STR + R
+        chw = irh * irw if ci else TH * TW
+        targs = f"{'true' if ci else 'false'}, {KK}, {TH}, {TW}, {R}, {S}, {STR}"
+        out += ["template <>", f"struct BwwJtBlocks<{targs}> {{", "    static constexpr bool available = true;",
+                "    template <int W>", "    struct Word;", "};"]
+        for w in range((chw + 31) // 32):
+            out += ["template <>", f"struct BwwJtBlocks<{targs}>::Word<{w}> {{",
+                    "    template <class Acc, class Ov>",
+                    "    static __device__ __forceinline__ void run(Acc& acc, const Ov& O, float v, unsigned m) {",
+                    bww_word_asm(cfg, w), "    }", "};", ""]
     out += ["}  // namespace spc", ""]
     open(OUT, "w").write("\n".join(out))
     print("wrote", OUT, sum(len(x) for x in out), "bytes")

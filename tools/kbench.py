@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--config", default="cfg1_single3x3_b16")
     ap.add_argument("--sparsity", type=float, nargs="+", default=[0.5])
     ap.add_argument("--layers", type=int, default=99)
+    ap.add_argument("--bww-check", default="input")
     args = ap.parse_args()
     V = 16
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -41,7 +42,7 @@ def main():
             ops = {
                 "fwd": (sp.pack_act_nchwc(D, V), sp.pack_filter(G, V), sp.BwwCheck.input),
                 "bwi": (sp.pack_act_nchwc(dY, V), sp.pack_filter(G, V, True), sp.BwwCheck.input),
-                "bww": (sp.pack_act_chwnn(D, V), sp.pack_act_nchwc(dY, V), sp.BwwCheck.input),
+                "bww": ((sp.pack_act_chwnn(D, V), sp.pack_act_nchwc(dY, V), sp.BwwCheck.input) if args.bww_check == "input" else (sp.pack_act_nchwc(D, V), sp.pack_act_chwnn(dY, V), sp.BwwCheck.output_grad)),
             }
             row = []
             for name, (a, b, chk) in ops.items():
