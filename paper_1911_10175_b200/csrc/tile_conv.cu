@@ -113,16 +113,24 @@ struct ConvGeom {
     using AY = Axis<FWD, TH, S, STR>;
     using AX = Axis<FWD, TW, R, STR>;
     static constexpr int RH = AY::EXT, RWW = AX::EXT;         // one warp's region
-    static constexpr int YSTEP = FWD ? TH * STR : TH / STR;   // region offset between warp tiles
+    static constexpr int YSTEP = FWD ? TH * STR : TH / STR;   // source offset between warp tiles
     static constexpr int XSTEP = FWD ? TW * STR : TW / STR;
     static constexpr int NQ = (RWW + 3) / 4;                  // float4 chunks per warp region row
-    static constexpr int CRH = (NWY - 1) * YSTEP + RH;         // CTA region
+    static constexpr int RWWP = 4 * NQ;                        // padded row of a warp region
+    static constexpr int NW = NWY * NWX;
+    // SHARED: the warps' regions overlap inside one CTA region (halo staged
+    // once) -- possible when every warp's x offset keeps rows 16B-aligned.
+    // Otherwise each warp keeps its own padded copy (halos duplicated).
+    static constexpr bool SHARED = NWX == 1 || XSTEP % 4 == 0;
+    static constexpr int CRH = (NWY - 1) * YSTEP + RH;
     static constexpr int CRW = (NWX - 1) * XSTEP + RWW;
-    static constexpr int CRWP = ((NWX - 1) * XSTEP + 4 * NQ + 3) / 4 * 4;  // padded row (16B multiple)
-    static constexpr int PLANE = CRH * CRWP;
+    static constexpr int CRWP = ((NWX - 1) * XSTEP + RWWP + 3) / 4 * 4;
+    static constexpr int ROW = SHARED ? CRWP : RWWP;           // row stride inside a plane
+    static constexpr int WPLANE = RH * RWWP;                   // per-warp copy, one channel
+    static constexpr int PLANE = SHARED ? CRH * CRWP : NW * WPLANE;  // one channel
     static constexpr int RHW = RH * RWW;
     static constexpr int NWORD = (RHW + 31) / 32;
-    static constexpr int NT = NWY * NWX * 32;
+    static constexpr int NT = NW * 32;
     static constexpr int NST = 3;  // staging pipeline depth (channel blocks in flight)
     static constexpr int SMEM = NST * 16 * PLANE * 4;
 };
@@ -157,10 +165,9 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
     if (sel != nullptr && __ldg(sel) != want) return;
     using AY = typename Gm::AY;
     using AX = typename Gm::AX;
-    constexpr int RH = Gm::RH, RWW = Gm::RWW, NQ = Gm::NQ, CRH = Gm::CRH, CRW = Gm::CRW, CRWP = Gm::CRWP;
-    constexpr int PLANE = Gm::PLANE, RHW = Gm::RHW, NWORD = Gm::NWORD, NT = Gm::NT;
+    constexpr int RH = Gm::RH, RWW = Gm::RWW, NQ = Gm::NQ, ROW = Gm::ROW;
+    constexpr int PLANE = Gm::PLANE, WPLANE = Gm::WPLANE, RHW = Gm::RHW, NWORD = Gm::NWORD, NT = Gm::NT;
     constexpr int TAPS = R * S;
-    static_assert(Gm::XSTEP % 4 == 0 || NWX == 1, "warp regions must stay 16B aligned");
 
     // channel-major staging of the swept tensor: [buf][16 channels][CRH][CRWP]
     extern __shared__ __align__(16) float Ds[];
@@ -193,26 +200,44 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
     const float* fbase = filt + (size_t)(k0 / 16) * CiB * TAPS * 256 + (k0 % 16);
     const float* sbase = src + (size_t)i * CiB * Hs * Ws * 16;
 
-    // 4-byte cp.async transposes pixel-major global vectors into channel
-    // planes (zero-filled outside the image = virtual padding)
+    // 4-byte cp.async transposes pixel-major global vectors into per-warp
+    // channel planes (zero-filled outside the image = virtual padding):
+    // element (warp w, ry, rx, ch) -> Ds[buf][ch][w][ry][rx]
     auto stage = [&](int cb, int buf) {
         const float* sp = sbase + (size_t)cb * Hs * Ws * 16;
         const uint32_t d0 = smem_u32(Ds + buf * 16 * PLANE);
-        for (int idx = threadIdx.x; idx < CRH * CRW * 16; idx += NT) {
-            const int ch = idx & 15, p = idx >> 4;
-            const int ry = p / CRW, rx = p - ry * CRW;
-            const int gy = sy0 + ry, gx = sx0 + rx;
-            const bool ok = gy >= 0 && gy < Hs && gx >= 0 && gx < Ws;
-            const float* g = ok ? sp + ((size_t)gy * Ws + gx) * 16 + ch : sp;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
-                             d0 + (uint32_t)(ch * PLANE + ry * CRWP + rx) * 4u),
-                         "l"(g), "r"(ok ? 4 : 0));
+        if constexpr (Gm::SHARED) {
+            for (int idx = threadIdx.x; idx < Gm::CRH * Gm::CRW * 16; idx += NT) {
+                const int ch = idx & 15, p = idx >> 4;
+                const int ry = p / Gm::CRW, rx = p - ry * Gm::CRW;
+                const int gy = sy0 + ry, gx = sx0 + rx;
+                const bool ok = gy >= 0 && gy < Hs && gx >= 0 && gx < Ws;
+                const float* g = ok ? sp + ((size_t)gy * Ws + gx) * 16 + ch : sp;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                                 d0 + (uint32_t)(ch * PLANE + ry * ROW + rx) * 4u),
+                             "l"(g), "r"(ok ? 4 : 0));
+            }
+        } else {
+            for (int idx = threadIdx.x; idx < Gm::NW * RH * RWW * 16; idx += NT) {
+                const int ch = idx & 15;
+                int p = idx >> 4;
+                const int rx = p % RWW;
+                p /= RWW;
+                const int ry = p % RH;
+                const int w = p / RH;
+                const int gy = sy0 + (w / NWX) * Gm::YSTEP + ry, gx = sx0 + (w % NWX) * Gm::XSTEP + rx;
+                const bool ok = gy >= 0 && gy < Hs && gx >= 0 && gx < Ws;
+                const float* g = ok ? sp + ((size_t)gy * Ws + gx) * 16 + ch : sp;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                                 d0 + (uint32_t)(ch * PLANE + w * WPLANE + ry * ROW + rx) * 4u),
+                             "l"(g), "r"(ok ? 4 : 0));
+            }
         }
         cp_async_commit();
     };
 
     // this warp's region origin inside a channel plane
-    const int woff = wy * Gm::YSTEP * CRWP + wx * Gm::XSTEP;
+    const int woff = Gm::SHARED ? wy * Gm::YSTEP * ROW + wx * Gm::XSTEP : warp * WPLANE;
 
     // per-lane region pixels q = lane + 32w: plane offset and valid-tap
     // weight (number of (target, tap) pairs whose target is in the image)
@@ -225,7 +250,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         qoff[w] = woff;
         if (q < RHW) {
             const int ry = q / RWW, rx = q % RWW;
-            qoff[w] = woff + ry * CRWP + rx;
+            qoff[w] = woff + ry * ROW + rx;
 #pragma unroll
             for (int v = 0; v < S; ++v) {
                 const int t = AY::target(ry, v);
@@ -315,7 +340,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                 if (ry + 1 < RH) {
 #pragma unroll
                     for (int h = 0; h < NQ; ++h)
-                        nxt[h] = *reinterpret_cast<const float4*>(Pw + (ry + 1) * CRWP + 4 * h);
+                        nxt[h] = *reinterpret_cast<const float4*>(Pw + (ry + 1) * ROW + 4 * h);
                 }
 #pragma unroll
                 for (int rx = 0; rx < RWW; ++rx) {
@@ -453,6 +478,18 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
         SPC_VJ(23, 4, 4, 4, 2, 2, 1, 30)
         SPC_VJ(24, 4, 4, 8, 2, 1, 1, 30)
         SPC_VJ(25, 2, 4, 8, 2, 2, 1, 30)
+        SPC_V(26, 2, 4, 7, 2, 2, 1)
+        SPC_V(27, 2, 7, 4, 2, 2, 1)
+        SPC_V(28, 2, 7, 7, 2, 1, 1)
+        SPC_V(29, 4, 4, 7, 2, 1, 1)
+        SPC_V(30, 4, 7, 4, 2, 1, 1)
+        SPC_V(31, 2, 4, 7, 4, 1, 1)
+        SPC_V(32, 4, 2, 7, 2, 2, 1)
+        SPC_V(33, 2, 7, 7, 2, 2, 1)
+        SPC_V(34, 4, 4, 7, 2, 2, 1)
+        SPC_V(35, 4, 2, 7, 4, 1, 1)
+        SPC_VJ(36, 4, 7, 4, 2, 1, 1, 100)
+        SPC_VJ(37, 4, 4, 7, 2, 1, 1, 100)
         default: return cudaErrorInvalidValue;
     }
 #undef SPC_V
@@ -524,33 +561,31 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
 #define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
     return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st)
     if (sh.R == 3 && sh.O == 1) {
-        const int Ho = fwd ? sh.Hp : sh.H;
+        // tile choices from tools/tune.py sweeps over the VGG16 layers
+        // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
+        // resolution; KK=4 branches for sparse, the KK=4 4x8 jump table for
+        // density <= 15%, KK=2 7x7 for dense mode.
         if (sparse && kk4) {
-            // both kernels launch; the density probe's selector lets one run
             const int Ci = fwd ? sh.C : sh.K;
             const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
             int* sel = nullptr;
             cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
             if (e != cudaSuccess) return e;
             launch_density_probe(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel, st);
-            if (Ho <= 28)
-                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
-                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
-            else
-                e = fwd ? launch_cfg<true, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
-                        : launch_cfg<false, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
+            e = fwd ? launch_cfg<true, 4, 7, 4, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
+                    : launch_cfg<false, 4, 7, 4, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
             if (e == cudaSuccess)
                 e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1)
                         : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1);
             cudaFreeAsync(sel, st);
             return e;
         }
-        if (kk4 && !sparse) {
-            if (fwd) SPC_L(true, 4, 4, 8, 2, 1, 3, 1);
-            SPC_L(false, 4, 4, 8, 2, 1, 3, 1);
+        if (sparse) {
+            if (fwd) SPC_L(true, 2, 4, 8, 2, 2, 3, 1);
+            SPC_L(false, 2, 4, 8, 2, 2, 3, 1);
         }
-        if (fwd) SPC_L(true, 2, 4, 8, 2, 2, 3, 1);
-        SPC_L(false, 2, 4, 8, 2, 2, 3, 1);
+        if (fwd) SPC_L(true, 2, 7, 7, 2, 1, 3, 1);
+        SPC_L(false, 2, 7, 7, 2, 1, 3, 1);
     }
     if (sh.R == 3) {  // stride 2
         if (fwd) {

@@ -34,6 +34,8 @@ CONFIGS = [
     (True, 2, 4, 8, 3, 3, 1), (False, 2, 4, 8, 3, 3, 1),
     (True, 4, 4, 4, 3, 3, 1), (False, 4, 4, 4, 3, 3, 1),
     (True, 4, 4, 8, 3, 3, 1), (False, 4, 4, 8, 3, 3, 1),
+    (True, 4, 7, 4, 3, 3, 1), (False, 4, 7, 4, 3, 3, 1),
+    (True, 4, 4, 7, 3, 3, 1), (False, 4, 4, 7, 3, 3, 1),
 ]
 
 
