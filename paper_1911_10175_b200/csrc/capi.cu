@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "dispatch.h"
+#include "tile_bww.h"
 #include "tile_conv.h"
 
 namespace spc {
@@ -624,6 +625,20 @@ spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_
                                   const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
                                   void* stream) {
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    if (plan->comp == SPC_BWW) {
+        // src = input, filt = grad_out (spc_sparse_bww argument order)
+        spc_status s = validate_bww(src, filt, *shape, *plan);
+        if (s) return s;
+        if ((s = prepare_dst(*shape, *plan, dst))) return s;
+        if ((s = check_device())) return s;
+        cudaStream_t st = (cudaStream_t)stream;
+        if ((s = start_counters(*shape, *plan, mode, d_counters, st))) return s;
+        const bool ci = plan->check == SPC_CHECK_INPUT;
+        cudaError_t e = launch_tile_bww_variant(variant, ci, mode == SPC_SPARSE, make_dev_shape(*shape),
+                                                ci ? src->data : filt->data, ci ? filt->data : src->data, dst->data,
+                                                exec_slot(d_counters, mode), st);
+        return e == cudaSuccess ? SPC_OK : cuda_fail(e, "variant launch");
+    }
     const bool fwd = plan->comp == SPC_FWD;
     spc_status s = fwd ? validate_fwd(src, filt, *shape, *plan) : validate_bwi(src, filt, *shape, *plan);
     if (s) return s;

@@ -464,6 +464,40 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
     return e;
 }
 
+// Development entry: alternative BWW tile configurations (tools/tune.py --comp bww).
+cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, const DevShape& sh, const float* chk,
+                                    const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    const int Lc = check_input ? sh.K : sh.C, Mc = check_input ? sh.C : sh.K;
+    if (sh.R != 3 || sh.O != 1) return cudaErrorInvalidValue;
+#define SPC_BV(ID, CI, KK, CB, NWC, TH, TW)                                                                  \
+    case ID:                                                                                                 \
+        if (check_input != CI || Lc % (32 * KK) || Mc % (CB * NWC)) return cudaErrorInvalidValue;           \
+        return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, 3, 3, 1>(sparse, sh, chk, oth, dst, exec_ctr, st);
+    switch (variant) {
+        SPC_BV(0, true, 4, 1, 8, 4, 4)
+        SPC_BV(1, true, 4, 1, 4, 4, 4)
+        SPC_BV(2, true, 4, 1, 8, 4, 7)
+        SPC_BV(3, true, 4, 1, 8, 7, 4)
+        SPC_BV(4, true, 2, 2, 8, 4, 4)
+        SPC_BV(5, true, 2, 2, 8, 4, 7)
+        SPC_BV(6, true, 2, 2, 8, 7, 7)
+        SPC_BV(7, true, 4, 1, 8, 2, 4)
+        SPC_BV(8, true, 2, 1, 8, 7, 7)
+        SPC_BV(9, true, 4, 2, 4, 4, 4)
+        SPC_BV(10, true, 2, 4, 4, 4, 4)
+        SPC_BV(11, true, 4, 1, 8, 4, 8)
+        SPC_BV(12, true, 4, 1, 4, 4, 7)
+        SPC_BV(13, true, 2, 2, 4, 4, 7)
+        SPC_BV(20, false, 4, 1, 8, 2, 4)
+        SPC_BV(21, false, 2, 2, 8, 4, 4)
+        SPC_BV(22, false, 4, 1, 8, 4, 4)
+        SPC_BV(23, false, 2, 1, 8, 4, 7)
+        SPC_BV(24, false, 4, 1, 4, 2, 4)
+        default: return cudaErrorInvalidValue;
+    }
+#undef SPC_BV
+}
+
 bool tile_bww_supported(bool check_input, const DevShape& sh, int V) {
     if (V != 16) return false;
     const int Lc = check_input ? sh.K : sh.C, Mc = check_input ? sh.C : sh.K;
@@ -482,10 +516,11 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
     return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, STR>(sparse, sh, chk, oth, dst, exec_ctr, st)
     if (check_input) {
         if (sh.R == 3 && sh.O == 1) {
-            // the jump-table BWW variant (JTSEL) measured slower than per-pixel
-            // branches at every sparsity of the VGG sweep; branches only
-            if (kk4) SPC_B(true, 4, 1, 8, 4, 4, 3, 1);
-            SPC_B(true, 2, 2, 8, 4, 4, 3, 1);
+            // tools/tune.py --comp bww sweeps (profiles/r01_tune.md).  The
+            // jump-table BWW variant (JTSEL) measured slower than per-pixel
+            // branches at every sparsity of the VGG sweep; branches only.
+            if (kk4) SPC_B(true, 4, 1, 8, 7, 4, 3, 1);
+            SPC_B(true, 2, 2, 4, 4, 7, 3, 1);
         }
         if (sh.R == 3) {
             if (kk4) SPC_B(true, 4, 2, 4, 2, 4, 3, 2);
@@ -499,8 +534,7 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
         SPC_B(true, 2, 4, 4, 4, 8, 1, 2);
     }
     if (sh.R == 3 && sh.O == 1) {
-        if (kk4) SPC_B(false, 4, 1, 8, 2, 4, 3, 1);
-        SPC_B(false, 2, 2, 8, 4, 4, 3, 1);
+        SPC_B(false, 2, 1, 8, 4, 7, 3, 1);
     }
     if (sh.R == 3) {
         if (kk4) SPC_B(false, 4, 2, 4, 2, 2, 3, 2);

@@ -18,6 +18,7 @@ ap.add_argument("--comp", default="fwd")
 ap.add_argument("--sparsity", type=float, nargs="+", default=[0.0, 0.6, 0.9])
 ap.add_argument("--variants", type=int, nargs="+", default=list(range(14)))
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--check", default="input")
 a = ap.parse_args()
 L = sp._lib.load()
 V = 16
@@ -27,13 +28,19 @@ for li in a.layers:
     sh = wl.CONFIGS[a.config]()[li].shape
     G = wl.device_weights(sh.K, sh.C, sh.S, sh.R, g)
     for s in a.sparsity:
+        chk = sp.BwwCheck[a.check]
         if a.comp == "fwd":
             x = sp.pack_act_nchwc(wl.device_activation((sh.N, sh.C, sh.H, sh.W), s, g), V)
             y = sp.pack_filter(G, V)
+        elif a.comp == "bww":
+            Dd = wl.device_activation((sh.N, sh.C, sh.H, sh.W), s, g)
+            dY = wl.device_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), s, g)
+            x, y = ((sp.pack_act_chwnn(Dd, V), sp.pack_act_nchwc(dY, V)) if chk == sp.BwwCheck.input
+                    else (sp.pack_act_nchwc(Dd, V), sp.pack_act_chwnn(dY, V)))
         else:
             x = sp.pack_act_nchwc(wl.device_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), s, g), V)
             y = sp.pack_filter(G, V, True)
-        pl = sp.plan(sh, sp.Component[a.comp], V)
+        pl = sp.plan(sh, sp.Component[a.comp], V, 30, chk)
         mode = 1 if s == 0.0 else 0
         ref = sp.PreparedPass(x, y, sh, pl, sp.RunMode(mode))
         ref.launch(st.cuda_stream)
