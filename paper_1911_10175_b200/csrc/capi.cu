@@ -535,6 +535,47 @@ spc_status spc_run_parallel(const spc_tensor* a, const spc_tensor* b, const spc_
 }
 
 // Host-buffer drop-in: validate, copy in, run, copy out, synchronize.
+//
+// Large calls are pipelined over batch chunks on three streams, so the copy
+// of chunk c+1 in, the kernels of chunk c and the copy of chunk c-1 out run
+// concurrently (two copy engines + SMs).  FWD/BWI chunks are image ranges
+// (per-image independent: results are bitwise those of the device call).
+// BWW chunks are whole 16-image blocks of the ActCHWNn tensor; each chunk's
+// dG is summed in fixed chunk order by sum_partials_kernel (deterministic;
+// the fp32 sum is regrouped relative to a single device call).
+__global__ void sum_partials_kernel(const float* __restrict__ part, int nparts, size_t n, float* __restrict__ out) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int c = 0; c < nparts; ++c) s += part[(size_t)c * n + e];
+        out[e] = s;
+    }
+}
+
+namespace {
+struct HostStreams {
+    int dev = -1;
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ready = nullptr;
+};
+thread_local HostStreams g_hs;
+
+spc_status host_streams(HostStreams*& hs) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_hs.dev != dev) {
+        for (auto& st : g_hs.s) {
+            cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "stream create");
+        }
+        cudaError_t e = cudaEventCreateWithFlags(&g_hs.ready, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "event create");
+        g_hs.dev = dev;
+    }
+    hs = &g_hs;
+    return SPC_OK;
+}
+}  // namespace
+
 spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters) {
     if (!a || !b || !shape || !plan || !dst) return fail(SPC_ERR_ARG, "null argument");
@@ -546,44 +587,126 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     default: return fail(SPC_ERR_PLAN, "run_parallel: bad component");
     }
     if (st) return st;
+    if (mode != SPC_SPARSE && mode != SPC_DENSE) return fail(SPC_ERR_ARG, "bad run mode");
     spc_tensor out = *dst;
     if ((st = prepare_dst(*shape, *plan, &out))) return st;
     if ((st = check_device())) return st;
-    static thread_local cudaStream_t s_stream = nullptr;
-    static thread_local int s_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!s_stream || s_dev != dev) {
-        cudaError_t e = cudaStreamCreateWithFlags(&s_stream, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return cuda_fail(e, "stream create");
-        s_dev = dev;
-    }
-    cudaStream_t sm = s_stream;
-    float *da = nullptr, *db = nullptr, *dd = nullptr;
+    HostStreams* hs = nullptr;
+    if ((st = host_streams(hs))) return st;
+    cudaStream_t s0 = hs->s[0];
+
+    const bool bww = plan->comp == SPC_BWW;
+    const int V = plan->V;
+    const bool on_input = plan->check == SPC_CHECK_INPUT;
+    // the batch-sliced operands: FWD/BWI a; BWW both (checked in CHWNn blocks)
+    const spc_tensor* chk = bww ? (on_input ? a : b) : a;
+    const spc_tensor* oth = bww ? (on_input ? b : a) : nullptr;
+    const size_t io_bytes = (a->numel + b->numel + out.numel) * sizeof(float);
+    const int units = bww ? (shape->N + V - 1) / V : shape->N;  // chunk granularity
+    int nc = io_bytes >= (size_t)64 << 20 ? (io_bytes >= (size_t)512 << 20 ? 8 : 4) : 1;
+    if (nc > units) nc = units;
+
+    float *da = nullptr, *db = nullptr, *dd = nullptr, *dpart = nullptr;
     spc_counters* dc = nullptr;
     cudaError_t e;
-    if ((e = cudaMallocAsync((void**)&da, a->numel * sizeof(float), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&db, b->numel * sizeof(float), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&dd, out.numel * sizeof(float), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&dc, sizeof(spc_counters), sm)) != cudaSuccess) return cuda_fail(e, "alloc");
-    cudaMemcpyAsync(da, a->data, a->numel * sizeof(float), cudaMemcpyHostToDevice, sm);
-    cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, sm);
-    spc_tensor ta = *a, tb = *b, td = out;
-    ta.data = da;
-    tb.data = db;
-    td.data = dd;
-    st = spc_run_parallel(&ta, &tb, shape, plan, mode, &td, counters ? dc : nullptr, sm);
-    if (st == SPC_OK) {
-        cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, sm);
-        if (counters) cudaMemcpyAsync(counters, dc, sizeof(spc_counters), cudaMemcpyDeviceToHost, sm);
+    if ((e = cudaMallocAsync((void**)&da, a->numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if ((e = cudaMallocAsync((void**)&db, b->numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if ((e = cudaMallocAsync((void**)&dd, out.numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if ((e = cudaMallocAsync((void**)&dc, nc * sizeof(spc_counters), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
+    if (bww && nc > 1 &&
+        (e = cudaMallocAsync((void**)&dpart, (size_t)nc * out.numel * sizeof(float), s0)) != cudaSuccess)
+        return cuda_fail(e, "alloc");
+    // operands that are not batch-sliced go first, on s0
+    if (!bww) cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, s0);
+    cudaEventRecord(hs->ready, s0);  // allocations (+ filter) visible to the other streams
+
+    const float* hchk = chk->data;
+    float* dchk = chk == a ? da : db;
+    const float* hoth = oth ? oth->data : nullptr;
+    float* doth = oth ? (oth == a ? da : db) : nullptr;
+    const size_t chk_unit = chk->numel / units;                // per image (NCHWc) or per block (CHWNn)
+    const size_t oth_unit = oth ? oth->numel / shape->N : 0;   // per image (NCHWc)
+    const size_t out_unit = bww ? 0 : out.numel / shape->N;    // per image
+
+    for (int c = 0; c < nc && st == SPC_OK; ++c) {
+        cudaStream_t sc = hs->s[c % 3];
+        cudaStreamWaitEvent(sc, hs->ready, 0);
+        const int u0 = (int)((long)units * c / nc), u1 = (int)((long)units * (c + 1) / nc);
+        const int i0 = bww ? u0 * V : u0;
+        const int i1 = bww ? (u1 * V < shape->N ? u1 * V : shape->N) : u1;
+        spc_shape shc = *shape;
+        shc.N = i1 - i0;
+        // H2D of this chunk's slices
+        cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
+                        (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sc);
+        if (oth)
+            cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
+                            (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sc);
+        // chunk tensor descriptors
+        spc_tensor tchk = *chk, toth, tb = *b, td = out;
+        tchk.data = dchk + (size_t)u0 * chk_unit;
+        tchk.n = shc.N;
+        tchk.numel = (size_t)(u1 - u0) * chk_unit;
+        if (oth) {
+            toth = *oth;
+            toth.data = doth + (size_t)i0 * oth_unit;
+            toth.n = shc.N;
+            toth.numel = (size_t)(i1 - i0) * oth_unit;
+        }
+        if (bww) {
+            td.data = nc > 1 ? dpart + (size_t)c * out.numel : dd;
+            const spc_tensor* in_t = on_input ? &tchk : &toth;
+            const spc_tensor* dy_t = on_input ? &toth : &tchk;
+            st = spc_sparse_bww(in_t, dy_t, &shc, plan, mode, &td, counters ? dc + c : nullptr, sc);
+        } else {
+            tb.data = db;
+            td.data = dd + (size_t)i0 * out_unit;
+            td.numel = (size_t)(i1 - i0) * out_unit;
+            st = plan->comp == SPC_FWD ? spc_sparse_fwd(&tchk, &tb, &shc, plan, mode, &td, counters ? dc + c : nullptr, sc)
+                                       : spc_sparse_bwi(&tchk, &tb, &shc, plan, mode, &td, counters ? dc + c : nullptr, sc);
+            if (st == SPC_OK)
+                cudaMemcpyAsync(out.data + (size_t)i0 * out_unit, td.data, td.numel * sizeof(float),
+                                cudaMemcpyDeviceToHost, sc);
+        }
     }
-    cudaFreeAsync(da, sm);
-    cudaFreeAsync(db, sm);
-    cudaFreeAsync(dd, sm);
-    cudaFreeAsync(dc, sm);
-    e = cudaStreamSynchronize(sm);
+    if (st == SPC_OK && bww) {
+        // join the chunks on s0, reduce in fixed order, copy dG out
+        for (int c = 1; c < nc && c < 3; ++c) {
+            cudaEvent_t ev;
+            cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            cudaEventRecord(ev, hs->s[c]);
+            cudaStreamWaitEvent(s0, ev, 0);
+            cudaEventDestroy(ev);
+        }
+        if (nc > 1) {
+            sum_partials_kernel<<<grid_for(out.numel), 256, 0, s0>>>(dpart, nc, out.numel, dd);
+            note_launch();
+        }
+        cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0);
+    }
+    spc_counters hc[8];
+    if (st == SPC_OK && counters) {
+        for (int c = 0; c < nc; ++c)
+            cudaMemcpyAsync(&hc[c], dc + c, sizeof(spc_counters), cudaMemcpyDeviceToHost, hs->s[c % 3]);
+    }
+    for (int c = 0; c < 3; ++c) cudaStreamSynchronize(hs->s[c]);
+    cudaFreeAsync(da, s0);
+    cudaFreeAsync(db, s0);
+    cudaFreeAsync(dd, s0);
+    cudaFreeAsync(dc, s0);
+    if (dpart) cudaFreeAsync(dpart, s0);
+    e = cudaStreamSynchronize(s0);
     if (st) return st;
     if (e != cudaSuccess) return cuda_fail(e, "host run");
+    if (counters) {
+        std::memset(counters, 0, sizeof(*counters));
+        for (int c = 0; c < nc; ++c) {
+            counters->checked_vectors += hc[c].checked_vectors;
+            counters->executed_vector_fmas += hc[c].executed_vector_fmas;
+            counters->output_vector_loads += hc[c].output_vector_loads;
+            counters->output_vector_stores += hc[c].output_vector_stores;
+        }
+    }
     *dst = out;
     return SPC_OK;
 }

@@ -407,3 +407,23 @@ def test_cxx_dropin_matches_reference_library():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+def test_host_path_pipelined_chunks_match_device_path(sp):
+    """Large host-buffer calls run in pipelined batch chunks: FWD/BWI stay
+    bitwise equal to the device call; BWW (16-image-block chunks summed in
+    fixed order) stays within rounding of it, counters exact."""
+    V = 16
+    sh = sp.ConvShape.make(40, 64, 128, 56, 56, 3, 3, 1, 1)  # > 64 MB of host I/O per call
+    for comp, check in ALL:
+        a, b, ba, bb = make_inputs(sp, sh, comp, check, 0.6, V, 11)
+        pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
+        rd = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse)
+        ha, hb = ba.to(None), bb.to(None)
+        rh = sp.run_parallel(ha, hb, sh, pl, sp.RunMode.sparse)
+        got, ref = rh.out.data, rd.out.data.cpu().numpy()
+        if comp == 2:
+            assert O.max_abs_rel(got, ref) <= 1e-6
+        else:
+            assert np.array_equal(got, ref)
+        assert rh.counters == rd.counters
