@@ -490,6 +490,12 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
         SPC_V(35, 4, 2, 7, 4, 1, 1)
         SPC_VJ(36, 4, 7, 4, 2, 1, 1, 100)
         SPC_VJ(37, 4, 4, 7, 2, 1, 1, 100)
+        SPC_V(38, 4, 7, 4, 2, 1, 0)
+        SPC_V(39, 4, 4, 7, 2, 1, 0)
+        SPC_VJ(40, 4, 4, 8, 2, 2, 0, 100)
+        SPC_VJ(41, 4, 4, 8, 1, 1, 1, 100)
+        SPC_V(42, 4, 7, 4, 1, 1, 1)
+        SPC_V(43, 4, 7, 4, 4, 1, 0)
         default: return cudaErrorInvalidValue;
     }
 #undef SPC_V
@@ -572,8 +578,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
             if (e != cudaSuccess) return e;
             launch_density_probe(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel, st);
-            e = fwd ? launch_cfg<true, 4, 7, 4, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
-                    : launch_cfg<false, 4, 7, 4, 2, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
+            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
+                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
             if (e == cudaSuccess)
                 e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1)
                         : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1);
