@@ -43,6 +43,17 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# The result line goes to the real stdout; anything native libraries write to
+# file descriptor 1 (e.g. NCCL's version banner) is redirected to stderr so the
+# driver always sees exactly one JSON line.
+_RESULT_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(obj):
+    os.write(_RESULT_FD, (json.dumps(obj) + "\n").encode())
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -143,7 +154,7 @@ def run_reference_arm(args):
     import oracle
     from paper_1911_10175_b200 import workloads as wl
     if not oracle.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libspconv_ref.so was not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libspconv_ref.so was not built"})
         return
     layers = wl.CONFIGS[args.config]()
     workers = os.cpu_count() or 1
@@ -167,7 +178,7 @@ def run_reference_arm(args):
                          "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def config_dict(args, ws):
@@ -209,7 +220,11 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    # under torchrun (any world size) the collective path is live: NCCL
+    # process group, per-layer dG allreduce on a comm stream, barriers and
+    # max-over-ranks timing -- so a 1-GPU torchrun run exercises it too
+    distributed = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     V = 16
     layers = wl.CONFIGS[args.config]()
@@ -244,7 +259,7 @@ def main():
     log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s, {len(work)} passes/step, "
         f"{torch.cuda.memory_allocated(dev) / 2**30:.1f} GiB resident")
 
-    comm_stream = torch.cuda.Stream(device=dev) if ws > 1 else None
+    comm_stream = torch.cuda.Stream(device=dev) if distributed else None
 
     def step(events=None):
         for idx, (s, li, name, pp, _) in enumerate(work):
@@ -253,7 +268,7 @@ def main():
             pp.launch(sptr)
             if events is not None:
                 events[idx][1].record(stream)
-            if ws > 1 and name == "bww":
+            if distributed and name == "bww":
                 # BWW weight-gradient exchange: NCCL allreduce (sum) over NVLink,
                 # on a comm stream so it overlaps the next layer's passes
                 ev = torch.cuda.Event()
@@ -261,7 +276,7 @@ def main():
                 comm_stream.wait_event(ev)
                 with torch.cuda.stream(comm_stream):
                     dist.all_reduce(pp.out)
-        if ws > 1:
+        if distributed:
             stream.wait_stream(comm_stream)
 
     # warmup (also validates every pass once, counters read back)
@@ -275,7 +290,7 @@ def main():
     peak = ffma_peak(sp, dev, sptr)
 
     # ---------------- timed region
-    if ws > 1:
+    if distributed:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -296,7 +311,7 @@ def main():
         per_launch_ms[idx] = a.elapsed_time(b)  # last step's per-pass durations
     total_ms = e_start.elapsed_time(e_stop)
     clocks.stop()
-    if ws > 1:
+    if distributed:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -353,10 +368,10 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, layers)
     if not args.no_e2e:
-        out["e2e"] = e2e(args, sp, work, ws, rank)
+        out["e2e"] = e2e(args, sp, work, ws, rank, distributed)
     if rank == 0:
-        print(json.dumps(out), flush=True)
-    if ws > 1:
+        emit(out)
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -432,7 +447,7 @@ def cpu_baseline(args, layers):
                       f"run_parallel, backend automatic, {workers} workers"}
 
 
-def e2e(args, sp, work, ws, rank):
+def e2e(args, sp, work, ws, rank, distributed=False):
     """Same metric through the host-buffer C ABI (spc_run_parallel_host):
     pinned host inputs -> H2D -> kernels -> D2H of every output, per call."""
     import torch
@@ -464,7 +479,7 @@ def e2e(args, sp, work, ws, rank):
     for _ in range(args.e2e_steps):
         one_step()
     secs = (time.perf_counter() - t0) / args.e2e_steps
-    if ws > 1:
+    if distributed:
         import torch.distributed as dist
         t = torch.tensor([secs], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
