@@ -181,9 +181,20 @@ def run_reference_arm(args):
     emit(out)
 
 
+WORKLOAD_NAMES = {
+    "vgg16_b32": "VGG16 non-initial 3x3 convs (12 layers) x FWD/BWI/BWW",
+    "cfg1_single3x3_b16": "single 3x3 conv N=16 C=K=64 56x56 x FWD/BWI/BWW",
+    "resnet34_b64": "ResNet-34 3x3 convs + 1x1 s2 projections (35 layers) x FWD/BWI/BWW",
+    "resnet50_b64": "ResNet-50 v1.5 bottleneck convs (52 layers) x FWD/BWI/BWW",
+    "fixup_resnet50_b256": "Fixup ResNet-50 conv stack (52 layers, batch 256) x FWD/BWI/BWW",
+}
+
+
 def config_dict(args, ws):
-    return {"workload": f"{args.config}: VGG16 non-initial 3x3 convs (12 layers) x FWD/BWI/BWW",
-            "global_batch": 32 * ws, "per_gpu_batch": 32, "resolution": 224, "vector_width": 16,
+    from paper_1911_10175_b200 import workloads as wl
+    n = wl.CONFIGS[args.config]()[0].shape.N
+    return {"workload": f"{args.config}: {WORKLOAD_NAMES.get(args.config, args.config)}",
+            "global_batch": n * ws, "per_gpu_batch": n, "resolution": 224, "vector_width": 16,
             "sparsity_grid": list(args.grid), "bww_check": "input",
             "parallelism": f"dp{ws} (batch-sharded, BWW dG allreduce)",
             "l2": "inputs larger than L2 (step working set ~25 GB, each tensor touched once per step)"}
@@ -442,7 +453,7 @@ def cpu_baseline(args, layers):
     workers = os.cpu_count() or 1
     f, s = reference_sample(layers, args.grid, args.cpu_images, workers)
     return {"value": round(f / s / 1e9, 3), "unit": "GFLOP/s", "cores": workers, "kind": "reference",
-            "sample": f"{args.cpu_images} image(s) per layer x 12 VGG16 layers x FWD/BWI/BWW x sparsity "
+            "sample": f"{args.cpu_images} image(s) per layer x {len(layers)} layers of {args.config} x FWD/BWI/BWW x sparsity "
                       f"{list(args.grid)} ({f / 1e9:.0f} dense-equiv GFLOP in {s:.1f} s); reference "
                       f"run_parallel, backend automatic, {workers} workers"}
 

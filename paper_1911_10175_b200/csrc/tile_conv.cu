@@ -444,6 +444,28 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
 cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const DevShape& sh, const float* src,
                                      const float* filt, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
     const int Co = fwd ? sh.K : sh.C;
+    if (variant >= 50) {  // 1x1 stride 1 variants
+        if (sh.R != 1 || sh.O != 1) return cudaErrorInvalidValue;
+#define SPC_V1(ID, KK, TH, TW, NWY, NWX)                                                                        \
+    case ID:                                                                                                    \
+        if (Co % (32 * KK)) return cudaErrorInvalidValue;                                                       \
+        return fwd ? launch_cfg<true, KK, TH, TW, NWY, NWX, 1, 1, 1, 1, 0>(sparse, sh, src, filt, dst, exec_ctr, st) \
+                   : launch_cfg<false, KK, TH, TW, NWY, NWX, 1, 1, 1, 1, 0>(sparse, sh, src, filt, dst, exec_ctr, st);
+        switch (variant) {
+            SPC_V1(50, 4, 4, 8, 2, 1)
+            SPC_V1(51, 2, 4, 8, 2, 1)
+            SPC_V1(52, 8, 4, 4, 2, 1)
+            SPC_V1(53, 8, 2, 8, 2, 1)
+            SPC_V1(54, 8, 2, 4, 2, 2)
+            SPC_V1(55, 4, 7, 4, 1, 1)
+            SPC_V1(56, 8, 7, 2, 1, 1)
+            SPC_V1(57, 8, 4, 4, 1, 1)
+            SPC_V1(58, 4, 4, 8, 1, 1)
+            SPC_V1(59, 8, 7, 2, 2, 1)
+            default: return cudaErrorInvalidValue;
+        }
+#undef SPC_V1
+    }
     if (sh.R != 3 || sh.O != 1) return cudaErrorInvalidValue;
 #define SPC_V(ID, KK, TH, TW, NWY, NWX, GPF) SPC_VJ(ID, KK, TH, TW, NWY, NWX, GPF, 0)
 #define SPC_VJ(ID, KK, TH, TW, NWY, NWX, GPF, JT)                                                               \

@@ -427,3 +427,42 @@ def test_host_path_pipelined_chunks_match_device_path(sp):
         else:
             assert np.array_equal(got, ref)
         assert rh.counters == rd.counters
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("cfg,idx", [("resnet50_b64", 1), ("resnet50_b64", 2), ("resnet50_b64", 11),
+                                     ("resnet34_b64", 7), ("resnet34_b64", 8), ("vgg16_b32", 8)])
+def test_baseline_layers_match_reference_cpu(sp, cfg, idx):
+    """BASELINE layer geometries (stride-2 3x3, 1x1 reduce/expand/projection,
+    VGG 512-channel) at full spatial size and a 4-image batch: GPU vs the
+    reference's own CPU kernels on identical inputs, all three passes."""
+    import torch
+    from paper_1911_10175_b200 import workloads as wl
+    V = 16
+    sh = wl.CONFIGS[cfg]()[idx].shape.with_batch(4)
+    t = sh.astuple()
+    rng = np.random.default_rng(idx)
+    D = wl.host_activation((sh.N, sh.C, sh.H, sh.W), 0.6, rng)
+    G = wl.host_weights(sh.K, sh.C, sh.S, sh.R, rng)
+    dY = wl.host_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), 0.6, rng)
+    for comp, check, a, b in ((0, 0, D, G), (1, 0, dY, G), (2, 0, D, dY), (2, 1, D, dY)):
+        r = O.RefRun(comp, check, t, V, a, b)
+        r.exec(0, os.cpu_count() or 1)
+        ref_out, ref_cnt, _ = r.result()
+        ta, tb = torch.from_numpy(r.operand(0)).cuda(), torch.from_numpy(r.operand(1)).cuda()
+        if comp == 0:
+            ba = sp.BlockedTensor(sp.Layout.act_nchwc, V, sh.N, sh.C, sh.H, sh.W, data=ta)
+            bb = sp.BlockedTensor(sp.Layout.filter_kcrs_blk, V, k=sh.K, c=sh.C, s=sh.S, r=sh.R, data=tb)
+        elif comp == 1:
+            ba = sp.BlockedTensor(sp.Layout.act_nchwc, V, sh.N, sh.K, sh.out_h(), sh.out_w(), data=ta)
+            bb = sp.BlockedTensor(sp.Layout.filter_kcrs_blk, V, k=sh.C, c=sh.K, s=sh.S, r=sh.R, data=tb)
+        else:
+            la = sp.Layout.act_chwnn if check == 0 else sp.Layout.act_nchwc
+            lb = sp.Layout.act_nchwc if check == 0 else sp.Layout.act_chwnn
+            ba = sp.BlockedTensor(la, V, sh.N, sh.C, sh.H, sh.W, data=ta)
+            bb = sp.BlockedTensor(lb, V, sh.N, sh.K, sh.out_h(), sh.out_w(), data=tb)
+        _, res, got = run(sp, sh, comp, check, V, ba, bb, 0)
+        assert O.max_abs_rel(got, ref_out) <= TOL, (cfg, idx, comp, check)
+        assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
+        assert res.counters.checked_vectors == ref_cnt["checked_vectors"]
+        r.close()
