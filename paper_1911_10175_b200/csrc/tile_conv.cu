@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                                                                    const float* __restrict__ filt,
                                                                    float* __restrict__ dst,
                                                                    unsigned long long* __restrict__ exec_ctr,
-                                                                   const int* __restrict__ sel, int want) {
+                                                                   const int* __restrict__ sel, int want,
+                                                                   int group_fastest) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     // device-side kernel choice (see launch_tile_conv): the variant whose
     // selector value does not match exits before touching memory
@@ -181,10 +182,15 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wy = warp / NWX, wx = warp % NWX;
     const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
-    // blockIdx.x = tile * groups + channel group: the CTAs that share a source
-    // region run back to back, so the second read of it hits L2
+    // block order: group_fastest -> blockIdx.x = tile * groups + group, so the
+    // CTAs that share a source region run back to back (its second read hits
+    // L2; used when the source tensor is larger than L2 wants); otherwise
+    // tile-fastest, so co-resident CTAs share a channel group's filter lines
+    // in L1 (used when the source fits in L2 anyway)
     const int ngroups = Co / (32 * KK);
-    const int kg = blockIdx.x % ngroups, tile = blockIdx.x / ngroups;
+    const int ntile = gridDim.x / ngroups;
+    const int kg = group_fastest ? blockIdx.x % ngroups : blockIdx.x / ntile;
+    const int tile = group_fastest ? blockIdx.x / ngroups : blockIdx.x % ntile;
     const int ty_idx = tile / tiles_x, tx_idx = tile % tiles_x;
     const int yc0 = ty_idx * TH * NWY, xc0 = tx_idx * TW * NWX;  // target origin of the CTA
     const int y0 = yc0 + wy * TH, x0 = xc0 + wx * TW;              // target origin of this warp
@@ -433,7 +439,11 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
         cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
         attr_set = true;
     }
-    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want);
+    const int Ci = FWD ? sh.C : sh.K;
+    const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
+    const size_t src_bytes = (size_t)sh.N * Ci * Hs * Ws * sizeof(float);
+    const int group_fastest = src_bytes > ((size_t)48 << 20) ? 1 : 0;
+    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest);
     note_launch();
     return cudaGetLastError();
 }
