@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspconv_b200.so")
+# SPC_LIB_PATH: alternative build of the same library (A/B timing in tools/)
+LIB_PATH = os.environ.get("SPC_LIB_PATH") or os.path.join(HERE, "libspconv_b200.so")
 
 SPC_OK, SPC_ERR_SHAPE, SPC_ERR_PLAN, SPC_ERR_LAYOUT, SPC_ERR_ARG, SPC_ERR_CUDA, SPC_ERR_NCCL, SPC_ERR_NO_DEVICE = range(8)
 STATUS_NAMES = {0: "SPC_OK", 1: "SPC_ERR_SHAPE", 2: "SPC_ERR_PLAN", 3: "SPC_ERR_LAYOUT", 4: "SPC_ERR_ARG",

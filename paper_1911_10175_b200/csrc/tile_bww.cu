@@ -338,6 +338,15 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
                             const float4 q4 = cur[rx >> 2];
                             const float d =
                                 (rx & 3) == 0 ? q4.x : (rx & 3) == 1 ? q4.y : (rx & 3) == 2 ? q4.z : q4.w;
+                            int ntap = 0;  // folds to a constant per unrolled pixel
+#pragma unroll
+                            for (int v = 0; v < S; ++v)
+#pragma unroll
+                                for (int u = 0; u < R; ++u) {
+                                    const int ny = ry - v, nx = rx - u;
+                                    ntap += !CHECK_INPUT || !(ny < 0 || nx < 0 || ny % STR || nx % STR ||
+                                                              ny / STR >= TH || nx / STR >= TW);
+                                }
 #pragma unroll
                             for (int v = 0; v < S; ++v) {
 #pragma unroll
@@ -352,9 +361,7 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
                                     } else {
                                         q = (ry * STR + v) * OTW + rx * STR + u;
                                     }
-#pragma unroll
-                                    for (int jj = 0; jj < KK; ++jj)
-                                        acc[cc][v * R + u][jj] = fmaf(d, O[q][jj], acc[cc][v * R + u][jj]);
+                                    fma_lane(acc[cc][v * R + u], d, O[q], ntap);
                                 }
                             }
                         }

@@ -84,6 +84,8 @@ struct FVec<8> {
     }
 };
 
+
+
 // Static geometry of one warp tile.  Target = output of the pass (Y for FWD,
 // dD for BWI); source = the swept tensor (D for FWD, dY for BWI).
 template <bool FWD, int T, int F, int STR>  // T = tile extent, F = filter extent
@@ -354,6 +356,11 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                     if (!SPARSE || ((m[p >> 5] >> (p & 31)) & 1u)) {
                         const float4 q4 = cur[rx >> 2];
                         const float d = (rx & 3) == 0 ? q4.x : (rx & 3) == 1 ? q4.y : (rx & 3) == 2 ? q4.z : q4.w;
+                        int ntap = 0;  // folds to a constant per unrolled pixel
+#pragma unroll
+                        for (int v = 0; v < S; ++v)
+#pragma unroll
+                            for (int u = 0; u < R; ++u) ntap += AY::target(ry, v) >= 0 && AX::target(rx, u) >= 0;
 #pragma unroll
                         for (int v = 0; v < S; ++v) {
                             const int ty = AY::target(ry, v);
@@ -362,9 +369,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                             for (int u = 0; u < R; ++u) {
                                 const int tx = AX::target(rx, u);
                                 if (tx < 0) continue;
-#pragma unroll
-                                for (int j = 0; j < KK; ++j)
-                                    acc[ty * TW + tx][j] = fmaf(d, g[v * R + u].v[j], acc[ty * TW + tx][j]);
+                                fma_lane(acc[ty * TW + tx], d, g[v * R + u].v, ntap);
                             }
                         }
                     }

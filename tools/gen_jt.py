@@ -19,9 +19,11 @@ kernel code around it (staging, masks, epilogue) is ordinary CUDA C++.
 Run:  python tools/gen_jt.py   (rewrites the header; `make` rebuilds).
 """
 import os
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_1911_10175_b200", "csrc", "jt_blocks.cuh")
+F32X2 = "--f32x2" in sys.argv
 
 # BWW: (CHECK_INPUT, KK, TH, TW, R, S, STR) -- per (checked channel, word)
 BWW_CONFIGS = [
@@ -71,9 +73,21 @@ def word_asm(cfg, w):
     gi = lambda f, j: NACC + f * KK + j
     V = NACC + TAPS * KK
     M = V + 1
+    # packed f32x2 FMAs: accumulator and tap channel pairs live in .b64
+    # registers (ptxas coalesces the packing movs away) and the pixel value is
+    # broadcast to both halves (the FFMA2 scalar-operand form)
+    # Off: measured 20-35% SLOWER on B200 -- inside the multi-block asm ptxas
+    # does not coalesce the .b64 pairs with the C++ accumulators and emits a
+    # MOV pair after every FFMA2 (tools/gen_jt.py --f32x2 to regenerate).
+    P2 = F32X2 and KK % 2 == 0
+    pk = []
+    if P2:
+        pk = [f".reg .b64 A<{NACC // 2}>, G<{TAPS * KK // 2}>, jdd;"]
+        pk += [f"mov.b64 A{a // 2}, {{%{a}, %{a + 1}}};" for a in range(0, NACC, 2)]
+        pk += [f"mov.b64 G{(i - NACC) // 2}, {{%{i}, %{i + 1}}};" for i in range(NACC, NACC + TAPS * KK, 2)]
     lines = ["{",
              ".reg .b32 jm, jt, jp, jn;",
-             ".reg .f32 jd, jdn;",
+             ".reg .f32 jd, jdn;"] + pk + [
              f"mov.b32 jm, %{M};",
              "brev.b32 jt, jm;", "clz.b32 jp, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
              f"shfl.sync.idx.b32 jd, %{V}, jp, 31, -1;",
@@ -88,6 +102,8 @@ def word_asm(cfg, w):
         ry, rx = divmod(p, RWW)
         lines += ["brev.b32 jt, jm;", "clz.b32 jn, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
                   f"shfl.sync.idx.b32 jdn, %{V}, jn, 31, -1;"]
+        if P2:
+            lines.append("mov.b64 jdd, {jd, jd};")
         for v in range(S):
             ty = ay.target(ry, v)
             if ty < 0:
@@ -97,11 +113,19 @@ def word_asm(cfg, w):
                 if tx < 0:
                     continue
                 t = ty * TW + tx
+                if P2:
+                    for j in range(0, KK, 2):
+                        a = t * KK + j
+                        lines.append(f"fma.rn.f32x2 A{a // 2}, jdd, G{(gi(v * R + u, j) - NACC) // 2}, A{a // 2};")
+                    continue
                 for j in range(KK):
                     a = t * KK + j
                     lines.append(f"fma.rn.f32 %{a}, jd, %{gi(v * R + u, j)}, %{a};")
         lines += ["mov.f32 jd, jdn;", "brx.idx.uni jn, Ljt;"]
-    lines += ["Lend:", "}"]
+    lines += ["Lend:"]
+    if P2:
+        lines += [f"mov.b64 {{%{a}, %{a + 1}}}, A{a // 2};" for a in range(0, NACC, 2)]
+    lines += ["}"]
     body = "\\n\\t".join(lines)
     outs = ", ".join(f'"+f"(acc[{t}][{j}])' for t in range(TH * TW) for j in range(KK))
     ins = ", ".join(f'"f"(g[{f}].v[{j}])' for f in range(TAPS) for j in range(KK)) + ', "f"(v), "r"(m)'
