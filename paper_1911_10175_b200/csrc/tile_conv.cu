@@ -24,6 +24,7 @@
 // that pixel) per channel block; the warp total x (2*KK vectors) is the
 // reference's count (P/src/kernel_impl.hpp:188-189) independent of tiling.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "jt_blocks.cuh"
@@ -83,6 +84,22 @@ struct FVec<8> {
         *(reinterpret_cast<float4*>(p) + 1) = make_float4(v[4], v[5], v[6], v[7]);
     }
 };
+
+// KK fp32 channels as KK/2 64-bit lanes (two channels each): the operand form
+// of the packed f32x2 jump-table blocks (JtBlocks2).
+template <int KK>
+struct FVecP {
+    unsigned long long p[KK / 2];
+    __device__ __forceinline__ void load(const float* q) {
+        static_assert(KK == 4, "FVecP: KK == 4 only");
+        asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(p[0]), "=l"(p[1]) : "l"(q));
+    }
+};
+__device__ __forceinline__ float2 unpack_f32x2(unsigned long long x) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(x));
+    return r;
+}
 
 
 
@@ -274,11 +291,18 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         nzc[w] = 0;
     }
 
-    float acc[TH * TW][KK];
+    // JTP: jump-table kernel with packed f32x2 blocks -- accumulators and taps
+    // live as 64-bit channel pairs for the whole pass (no in-line path)
+    using JB2 = JtBlocks2<FWD, KK, TH, TW, R, S, STR>;
+    constexpr bool JTP = SPARSE && JT >= 100 && SPC_FFMA2 && JB2::available;
+    constexpr int KA = JTP ? KK / 2 : KK;
+    using AccT = std::conditional_t<JTP, unsigned long long, float>;
+    using GV = std::conditional_t<JTP, FVecP<KK>, FVec<KK>>;
+    AccT acc[TH * TW][KA];
 #pragma unroll
     for (int t = 0; t < TH * TW; ++t)
 #pragma unroll
-        for (int j = 0; j < KK; ++j) acc[t][j] = 0.0f;
+        for (int j = 0; j < KA; ++j) acc[t][j] = AccT(0);
 
     constexpr int NST = Gm::NST;
     bool use_jt = JT >= 100;  // JT in 1..99: decided per block below, starting with branches
@@ -294,7 +318,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         __syncthreads();
         const float* fcb = fbase + (size_t)cb * TAPS * 256;
         int blk_nnz = 0;  // this warp's region nonzeros over the block (uniform)
-        FVec<KK> g[TAPS];
+        GV g[TAPS];
         if constexpr (GPF == 1) {
 #pragma unroll
             for (int f = 0; f < TAPS; ++f) g[f].load(fcb + f * 256);
@@ -303,7 +327,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 #pragma unroll 1
         for (int c = 0; c < 16; ++c) {
             const float* P = Ds + (cb % NST) * 16 * PLANE + c * PLANE;
-            FVec<KK> gn[GPF == 1 ? TAPS : 1];
+            GV gn[GPF == 1 ? TAPS : 1];
             if constexpr (GPF == 0) {
                 // this channel's taps: L1 hits (prefetched one channel ahead,
                 // shared by the CTA's warps), issued before the mask ballots so
@@ -336,6 +360,9 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 #pragma unroll
                 for (int w = 0; w < NWORD; ++w) blk_nnz += __popc(m[w]);
             }
+            if constexpr (JTP) {
+                jt_words<0, NWORD, JB2>(acc, g, vv, m);
+            } else {
             if (use_jt) {
                 if constexpr (SPARSE && JT > 0 && JB::available) jt_words<0, NWORD, JB>(acc, g, vv, m);
             } else {
@@ -380,6 +407,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                 }
             }
             }  // in-line path
+            }  // !JTP
             if constexpr (GPF == 1) {
                 if (c + 1 < 16) {
 #pragma unroll
@@ -410,7 +438,13 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
             if (x >= Wo) break;
             FVec<KK> o;
 #pragma unroll
-            for (int j = 0; j < KK; ++j) o.v[j] = acc[ty * TW + tx][j];
+            for (int j = 0; j < KK; ++j) {
+                if constexpr (JTP) {
+                    const float2 q = unpack_f32x2(acc[ty * TW + tx][j / 2]);
+                    o.v[j] = j & 1 ? q.y : q.x;
+                }
+                else o.v[j] = acc[ty * TW + tx][j];
+            }
             o.store(dst + ((((size_t)i * CoB + k0 / 16) * Ho + y) * Wo + x) * 16 + (k0 % 16));
         }
     }

@@ -63,6 +63,24 @@ class Axis:
         return t if 0 <= t < self.T else -1
 
 
+# Two-ahead dispatch: on entry to a pixel block the NEXT nonzero's index jn is
+# already known, so the jump-table load for the block's own brx (ptxas lowers
+# brx.idx to LDC + BRX) and the shfl of the next value issue at the top of the
+# block and overlap its FMAs; the block itself finds the next-next index.
+def dispatch_init(V):
+    return ["brev.b32 jt, jm;", "clz.b32 jp, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
+            "brev.b32 jt, jm;", "clz.b32 jn, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
+            f"shfl.sync.idx.b32 jd, %{V}, jp, 31, -1;"]
+
+
+def dispatch_block_head(V):
+    return [f"shfl.sync.idx.b32 jdn, %{V}, jn, 31, -1;",
+            "brev.b32 jt, jm;", "clz.b32 jq, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;"]
+
+
+DISPATCH_TAIL = ["mov.f32 jd, jdn;", "mov.b32 jp, jn;", "mov.b32 jn, jq;", "brx.idx.uni jp, Ljt;"]
+
+
 def word_asm(cfg, w):
     fwd, KK, TH, TW, R, S, STR = cfg
     ay, ax = Axis(fwd, TH, S, STR), Axis(fwd, TW, R, STR)
@@ -86,11 +104,9 @@ def word_asm(cfg, w):
         pk += [f"mov.b64 A{a // 2}, {{%{a}, %{a + 1}}};" for a in range(0, NACC, 2)]
         pk += [f"mov.b64 G{(i - NACC) // 2}, {{%{i}, %{i + 1}}};" for i in range(NACC, NACC + TAPS * KK, 2)]
     lines = ["{",
-             ".reg .b32 jm, jt, jp, jn;",
+             ".reg .b32 jm, jt, jp, jn, jq;",
              ".reg .f32 jd, jdn;"] + pk + [
-             f"mov.b32 jm, %{M};",
-             "brev.b32 jt, jm;", "clz.b32 jp, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
-             f"shfl.sync.idx.b32 jd, %{V}, jp, 31, -1;",
+             f"mov.b32 jm, %{M};"] + dispatch_init(V) + [
              "Ljt: .branchtargets " + ", ".join(f"Lb{i}" for i in range(32)) + ", Lend;",
              "brx.idx.uni jp, Ljt;"]
     for i in range(32):
@@ -100,8 +116,7 @@ def word_asm(cfg, w):
             lines.append("bra.uni Lend;")
             continue
         ry, rx = divmod(p, RWW)
-        lines += ["brev.b32 jt, jm;", "clz.b32 jn, jt;", "sub.u32 jt, jm, 1;", "and.b32 jm, jm, jt;",
-                  f"shfl.sync.idx.b32 jdn, %{V}, jn, 31, -1;"]
+        lines += dispatch_block_head(V)
         if P2:
             lines.append("mov.b64 jdd, {jd, jd};")
         for v in range(S):
@@ -121,7 +136,7 @@ def word_asm(cfg, w):
                 for j in range(KK):
                     a = t * KK + j
                     lines.append(f"fma.rn.f32 %{a}, jd, %{gi(v * R + u, j)}, %{a};")
-        lines += ["mov.f32 jd, jdn;", "brx.idx.uni jn, Ljt;"]
+        lines += DISPATCH_TAIL
     lines += ["Lend:"]
     if P2:
         lines += [f"mov.b64 {{%{a}, %{a + 1}}}, A{a // 2};" for a in range(0, NACC, 2)]
@@ -129,6 +144,57 @@ def word_asm(cfg, w):
     body = "\\n\\t".join(lines)
     outs = ", ".join(f'"+f"(acc[{t}][{j}])' for t in range(TH * TW) for j in range(KK))
     ins = ", ".join(f'"f"(g[{f}].v[{j}])' for f in range(TAPS) for j in range(KK)) + ', "f"(v), "r"(m)'
+    return f'    asm volatile("{body}"\n                 : {outs}\n                 : {ins});'
+
+
+def word_asm_pair(cfg, w):
+    """word_asm with packed f32x2 FMAs on 64-bit operands: the accumulators
+    and taps are passed as .b64 registers holding two fp32 channels each (the
+    kernel keeps them in that form for the whole pass), so ptxas needs no
+    packing moves; the pixel value is broadcast with mov.b64 {jd, jd}, which
+    ptxas folds into the FFMA2 scalar-operand form."""
+    fwd, KK, TH, TW, R, S, STR = cfg
+    ay, ax = Axis(fwd, TH, S, STR), Axis(fwd, TW, R, STR)
+    RH, RWW = ay.EXT, ax.EXT
+    RHW = RH * RWW
+    KP = KK // 2
+    NACC = TH * TW * KP
+    TAPS = R * S
+    gi = lambda f, j: NACC + f * KP + j
+    V = NACC + TAPS * KP
+    M = V + 1
+    lines = ["{",
+             ".reg .b32 jm, jt, jp, jn, jq;",
+             ".reg .f32 jd, jdn;",
+             ".reg .b64 jdd;",
+             f"mov.b32 jm, %{M};"] + dispatch_init(V) + [
+             "Ljt: .branchtargets " + ", ".join(f"Lb{i}" for i in range(32)) + ", Lend;",
+             "brx.idx.uni jp, Ljt;"]
+    for i in range(32):
+        p = 32 * w + i
+        lines.append(f"Lb{i}:")
+        if p >= RHW:
+            lines.append("bra.uni Lend;")
+            continue
+        ry, rx = divmod(p, RWW)
+        lines += ["mov.b64 jdd, {jd, jd};"] + dispatch_block_head(V)
+        for v in range(S):
+            ty = ay.target(ry, v)
+            if ty < 0:
+                continue
+            for u in range(R):
+                tx = ax.target(rx, u)
+                if tx < 0:
+                    continue
+                t = ty * TW + tx
+                for j in range(KP):
+                    a = t * KP + j
+                    lines.append(f"fma.rn.f32x2 %{a}, jdd, %{gi(v * R + u, j)}, %{a};")
+        lines += DISPATCH_TAIL
+    lines += ["Lend:", "}"]
+    body = "\\n\\t".join(lines)
+    outs = ", ".join(f'"+l"(acc[{t}][{j}])' for t in range(TH * TW) for j in range(KP))
+    ins = ", ".join(f'"l"(g[{f}].p[{j}])' for f in range(TAPS) for j in range(KP)) + ', "f"(v), "r"(m)'
     return f'    asm volatile("{body}"\n                 : {outs}\n                 : {ins});'
 
 
@@ -209,6 +275,29 @@ def main():
                     "    template <class Acc, class Gv>",
                     "    static __device__ __forceinline__ void run(Acc& acc, const Gv& g, float v, unsigned m) {",
                     word_asm(cfg, w), "    }", "};", ""]
+    out += ["// Pair form (KK % 4 == 0 configs): acc[t][KK/2] and tap vectors of .b64 lanes.",
+            "template <bool FWD, int KK, int TH, int TW, int R, int S, int STR>",
+            "struct JtBlocks2 {",
+            "    static constexpr bool available = false;",
+            "    template <int W>",
+            "    struct Word {",
+            "        template <class Acc, class Gv>",
+            "        static __device__ __forceinline__ void run(Acc&, const Gv&, float, unsigned) {}",
+            "    };",
+            "};", ""]
+    for cfg in CONFIGS:
+        fwd, KK, TH, TW, R, S, STR = cfg
+        if KK % 4:
+            continue
+        RHW = Axis(fwd, TH, S, STR).EXT * Axis(fwd, TW, R, STR).EXT
+        targs = f"{'true' if fwd else 'false'}, {KK}, {TH}, {TW}, {R}, {S}, {STR}"
+        out += ["template <>", f"struct JtBlocks2<{targs}> {{", "    static constexpr bool available = true;",
+                "    template <int W>", "    struct Word;", "};"]
+        for w in range((RHW + 31) // 32):
+            out += ["template <>", f"struct JtBlocks2<{targs}>::Word<{w}> {{",
+                    "    template <class Acc, class Gv>",
+                    "    static __device__ __forceinline__ void run(Acc& acc, const Gv& g, float v, unsigned m) {",
+                    word_asm_pair(cfg, w), "    }", "};", ""]
     out += ["template <bool CI, int KK, int TH, int TW, int R, int S, int STR>",
             "struct BwwJtBlocks {",
             "    static constexpr bool available = false;",
