@@ -17,6 +17,7 @@
  *   spc_native_backend_available <- native_backend_available  kernels.hpp:53
  *   spc_backend_name    <- conv_result::backend / backend_names  kernels.hpp:47-54
  *   spc_relu / spc_relu_grad_mask <- relu / relu_grad_mask  P/include/spconv/sparsity.hpp:14-18
+ *   spc_gen_sparse      <- spconv::gen_sparse    P/include/spconv/sparsity.hpp (P/src/sparsity.cpp:42-55)
  *
  * Conventions
  *   - Plain pointers and sizes only; no C++ types or exceptions cross the ABI.
@@ -139,6 +140,13 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
 /* ---- ReLU semantics on device (P/src/sparsity.cpp:11-28), bit-exact ---- */
 spc_status spc_relu(const float* in, float* out, size_t n, void* stream);
 spc_status spc_relu_grad_mask(const float* pre, const float* upstream, float* out, size_t n, void* stream);
+
+/* ---- synthetic inputs of the reference harness (host, no device needed) ---- */
+/* gen_sparse (P/src/sparsity.cpp:42-55): out[e] = 0 with probability
+ * `sparsity`, else U[0.1, 1], from std::mt19937_64(seed) through the
+ * reference's hand-mapped unit() (sparsity.cpp:34-38) -- the same stream, so
+ * the same tensor, as the reference's sweep/verify harness (bench.cpp:127-180). */
+spc_status spc_gen_sparse(float* out, size_t count, double sparsity, uint64_t seed);
 
 /* ---- device layout conversion: ActNCHWc -> ActCHWNn (tensor.cpp:94-108) ---- */
 spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stream);

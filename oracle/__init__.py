@@ -123,6 +123,15 @@ def ref():
         L.ref_blocked_output.restype = C.c_size_t
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_hardware_concurrency.restype = C.c_uint
+        L.ref_find_layer.argtypes = [C.c_char_p, _i32p]
+        L.ref_registry_name.argtypes = [C.c_int, C.c_char_p, C.c_size_t]
+        L.ref_scaled_shape.argtypes = [_i32p, C.c_int, C.c_int, _i32p]
+        L.ref_run_sweep.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int,
+                                    C.c_uint64, C.c_int, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t]
+        L.ref_format_csv.argtypes = [C.c_int, C.c_char_p, _i32p, C.POINTER(C.c_double), _i32p, _i32p,
+                                     C.POINTER(C.c_double), _u64p, C.POINTER(C.c_double),
+                                     C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t]
+        L.ref_load_curves.argtypes = [C.c_char_p]
         _ref = L
     return _ref
 
@@ -392,3 +401,60 @@ def ref_shape_make(N, Cc, K, H, W, R, S, O=1, P=1):
     if ref().ref_shape_make(N, Cc, K, H, W, R, S, O, P, out):
         raise ValueError(ref().ref_last_error().decode())
     return tuple(out)
+
+
+# ---------------------------------------------------------------- harness (bench.cpp / projector.cpp)
+def ref_registry() -> dict:
+    """name -> 11-int shape of the reference's layer registry (bench.cpp:21-52)."""
+    L = ref()
+    out = {}
+    for i in range(L.ref_registry_size()):
+        buf = C.create_string_buffer(64)
+        L.ref_registry_name(i, buf, 64)
+        sh = (C.c_int * 11)()
+        L.ref_find_layer(buf.value, sh)
+        out[buf.value.decode()] = tuple(sh)
+    return out
+
+
+def ref_scaled_shape(base, minibatch, scale):
+    out = (C.c_int * 11)()
+    if ref().ref_scaled_shape((C.c_int * 11)(*base), minibatch, scale, out):
+        raise ValueError(ref().ref_last_error().decode())
+    return tuple(out)
+
+
+def ref_run_sweep(layers, comps, grid, minibatch, scale, seed, repeats=1):
+    """The reference's run_sweep -> (sweep CSV, curves CSV) strings."""
+    mask = sum(1 << int(c) for c in comps)
+    g = (C.c_double * len(grid))(*grid)
+    a, b = C.create_string_buffer(1 << 20), C.create_string_buffer(1 << 20)
+    if ref().ref_run_sweep("\n".join(layers).encode(), mask, g, len(grid), minibatch, scale, int(seed), repeats,
+                           a, 1 << 20, b, 1 << 20):
+        raise ValueError(ref().ref_last_error().decode())
+    return a.value.decode(), b.value.decode()
+
+
+def ref_format_csv(records):
+    """write_sweep_csv / write_curves_csv of the given records (objects with
+    layer, comp, sparsity, mode, workers, median_ns, exec_fmas, speedup_vs_dense)."""
+    n = len(records)
+    comps = (C.c_int * n)(*[int(r.comp) for r in records])
+    sp = (C.c_double * n)(*[float(r.sparsity) for r in records])
+    modes = (C.c_int * n)(*[int(r.mode) for r in records])
+    wk = (C.c_int * n)(*[int(r.workers) for r in records])
+    ns = (C.c_double * n)(*[float(r.median_ns) for r in records])
+    fm = (C.c_uint64 * n)(*[int(r.exec_fmas) for r in records])
+    su = (C.c_double * n)(*[float(r.speedup_vs_dense) for r in records])
+    a, b = C.create_string_buffer(1 << 20), C.create_string_buffer(1 << 20)
+    if ref().ref_format_csv(n, "\n".join(r.layer for r in records).encode(), comps, sp, modes, wk, ns, fm, su,
+                            a, 1 << 20, b, 1 << 20):
+        raise ValueError(ref().ref_last_error().decode())
+    return a.value.decode(), b.value.decode()
+
+
+def ref_load_curves(path) -> int:
+    n = ref().ref_load_curves(str(path).encode())
+    if n < 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return n

@@ -9,13 +9,17 @@
 // (P/src/sparsity.cpp:42).  Nothing here re-implements reference arithmetic.
 #include <cstdint>
 #include <cstring>
+#include <sstream>
+#include <vector>
 #include <exception>
 #include <memory>
 #include <random>
 #include <string>
 #include <thread>
 
+#include "spconv/bench.hpp"
 #include "spconv/kernels.hpp"
+#include "spconv/projector.hpp"
 #include "spconv/oracle.hpp"
 #include "spconv/planner.hpp"
 #include "spconv/sparsity.hpp"
@@ -222,5 +226,110 @@ size_t ref_blocked_output(void* h, float* out) {
 void ref_free(void* h) { delete static_cast<prepared*>(h); }
 
 int ref_native_backend_available(int V) { return native_backend_available(V) ? 1 : 0; }
+
+
+// ---- harness (P/src/bench.cpp, P/src/projector.cpp) ----
+
+static int put_str(const std::string& s, char* out, size_t len) {
+    if (s.size() + 1 > len) { g_err = "buffer too small"; return 1; }
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+// layer_registry()/find_layer(): shape of the named layer (11 ints), -1 if unknown
+int ref_find_layer(const char* name, int* shape_out) {
+    const layer_config* lc = find_layer(name);
+    if (!lc) return -1;
+    const conv_shape& sh = lc->shape;
+    const int v[11] = {sh.N, sh.C, sh.K, sh.H, sh.W, sh.R, sh.S, sh.O, sh.P, sh.padW, sh.padH};
+    std::memcpy(shape_out, v, sizeof v);
+    return 0;
+}
+
+int ref_registry_size() { return int(layer_registry().size()); }
+
+int ref_registry_name(int i, char* out, size_t len) {
+    const auto& reg = layer_registry();
+    if (i < 0 || i >= int(reg.size())) return -1;
+    return put_str(reg[i].name, out, len);
+}
+
+int ref_scaled_shape(const int* base, int minibatch, int scale, int* out) {
+    try {
+        const conv_shape sh = scaled_shape(to_shape(base), minibatch, scale);
+        const int v[11] = {sh.N, sh.C, sh.K, sh.H, sh.W, sh.R, sh.S, sh.O, sh.P, sh.padW, sh.padH};
+        std::memcpy(out, v, sizeof v);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// run_sweep() with workers = 1 and the given request; both CSVs returned
+int ref_run_sweep(const char* layers_nl, int comps_mask, const double* grid, int ngrid, int minibatch, int scale,
+                  uint64_t seed, int repeats, char* sweep_csv, size_t sweep_len, char* curves_csv,
+                  size_t curves_len) {
+    try {
+        sweep_request req;
+        req.layers.clear();
+        std::istringstream ls(layers_nl);
+        for (std::string l; std::getline(ls, l);)
+            if (!l.empty()) req.layers.push_back(l);
+        req.comps.clear();
+        for (int c = 0; c < 3; ++c)
+            if (comps_mask >> c & 1) req.comps.push_back(component(c));
+        req.grid.assign(grid, grid + ngrid);
+        req.minibatch = minibatch;
+        req.scale = scale;
+        req.seed = seed;
+        req.repeats = repeats;
+        const auto recs = run_sweep(req);
+        std::ostringstream a, b;
+        write_sweep_csv(recs, a);
+        write_curves_csv(recs, b);
+        return put_str(a.str(), sweep_csv, sweep_len) || put_str(b.str(), curves_csv, curves_len);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// write_sweep_csv / write_curves_csv of caller-supplied records
+int ref_format_csv(int n, const char* layers_nl, const int* comps, const double* sparsity, const int* modes,
+                   const int* workers, const double* median_ns, const uint64_t* exec_fmas, const double* speedups,
+                   char* sweep_csv, size_t sweep_len, char* curves_csv, size_t curves_len) {
+    try {
+        std::vector<bench_record> recs(n);
+        std::istringstream ls(layers_nl);
+        for (int i = 0; i < n; ++i) {
+            std::getline(ls, recs[i].layer);
+            recs[i].comp = component(comps[i]);
+            recs[i].sparsity = sparsity[i];
+            recs[i].mode = run_mode(modes[i]);
+            recs[i].workers = workers[i];
+            recs[i].median_ns = median_ns[i];
+            recs[i].exec_fmas = exec_fmas[i];
+            recs[i].speedup_vs_dense = speedups[i];
+        }
+        std::ostringstream a, b;
+        write_sweep_csv(recs, a);
+        write_curves_csv(recs, b);
+        return put_str(a.str(), sweep_csv, sweep_len) || put_str(b.str(), curves_csv, curves_len);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// load_curves(): number of (layer, component) curves parsed, -1 on error
+int ref_load_curves(const char* path) {
+    try {
+        return int(load_curves(path).curves.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
 
 }  // extern "C"

@@ -68,6 +68,7 @@ _SIGS = {
     "spc_nchwc_to_chwnn": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.c_void_p]),
     "spc_ffma_peak_kernel": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_void_p]),
     "spc_l2_flush": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
+    "spc_gen_sparse": (C.c_int, [C.c_void_p, C.c_size_t, C.c_double, C.c_uint64]),
     "spc_debug_conv_variant": (C.c_int, [C.c_int, C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
                                          C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p,
                                          C.c_void_p]),

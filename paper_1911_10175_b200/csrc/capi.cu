@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <random>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -772,6 +773,20 @@ spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_
     cudaError_t e = launch_tile_conv_variant(variant, fwd, mode == SPC_SPARSE, make_dev_shape(*shape), src->data,
                                              filt->data, dst->data, exec_slot(d_counters, mode), st);
     return e == cudaSuccess ? SPC_OK : cuda_fail(e, "variant launch");
+}
+
+spc_status spc_gen_sparse(float* out, size_t count, double sparsity, uint64_t seed) {
+    if (!out && count) return fail(SPC_ERR_ARG, "null output");
+    if (!(sparsity >= 0.0 && sparsity <= 1.0)) return fail(SPC_ERR_ARG, "gen_sparse: sparsity must be in [0, 1]");
+    std::mt19937_64 rng(seed);
+    auto unit = [&] { return double(rng() >> 11) * 0x1p-53; };
+    for (size_t e = 0; e < count; ++e) {
+        if (unit() < sparsity)
+            out[e] = 0.0f;
+        else
+            out[e] = float(0.1 + 0.9 * unit());
+    }
+    return SPC_OK;
 }
 
 spc_status spc_l2_flush(float* scratch, size_t n, void* stream) {

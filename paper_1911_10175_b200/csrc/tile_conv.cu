@@ -85,6 +85,23 @@ struct FVec<8> {
     }
 };
 
+template <>
+struct FVec<16> {
+    float v[16];
+    __device__ __forceinline__ void load(const float* p) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(p) + h);
+            v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
+        }
+    }
+    __device__ __forceinline__ void store(float* p) const {
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+            *(reinterpret_cast<float4*>(p) + h) = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+    }
+};
+
 // KK fp32 channels as KK/2 64-bit lanes (two channels each): the operand form
 // of the packed f32x2 jump-table blocks (JtBlocks2).
 template <int KK>
@@ -511,6 +528,14 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
             SPC_V1(57, 8, 4, 4, 1, 1)
             SPC_V1(58, 4, 4, 8, 1, 1)
             SPC_V1(59, 8, 7, 2, 2, 1)
+            SPC_V1(60, 16, 2, 4, 1, 1)
+            SPC_V1(61, 16, 1, 8, 1, 1)
+            SPC_V1(62, 16, 2, 4, 2, 1)
+            SPC_V1(63, 16, 2, 4, 4, 1)
+            SPC_V1(64, 16, 1, 8, 4, 1)
+            SPC_V1(65, 8, 2, 8, 1, 1)
+            SPC_V1(66, 8, 4, 4, 4, 1)
+            SPC_V1(67, 16, 1, 7, 2, 1)
             default: return cudaErrorInvalidValue;
         }
 #undef SPC_V1
