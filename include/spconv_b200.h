@@ -133,6 +133,27 @@ spc_status spc_run_parallel(const spc_tensor* a, const spc_tensor* b, const spc_
                             const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
                             void* stream);
 
+/* ---- fused output epilogue for layer chains ----
+ * Applied per output element as the kernel writes it:
+ *   v = acc * alpha (+ add[i]);  if (relu) v = v > 0 ? v : 0;  if (mask) v = mask[i] > 0 ? v : 0
+ * i.e. the reference's relu / relu_grad_mask (P/src/sparsity.cpp:11-28) fused
+ * into FWD/BWI.  `add` and `mask` are DEVICE buffers with the output's layout
+ * and numel (ActNCHWc); NULL disables them.  {1, NULL, NULL, 0} = plain pass. */
+typedef struct {
+    float alpha;
+    const float* add;
+    const float* mask;
+    int relu;
+} spc_epilogue;
+spc_status spc_sparse_fwd_ex(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
+                             const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
+                             spc_counters* d_counters, void* stream);
+spc_status spc_sparse_bwi_ex(const spc_tensor* grad_out, const spc_tensor* filt_t, const spc_shape* shape,
+                             const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
+                             spc_counters* d_counters, void* stream);
+/* The same epilogue as a standalone pass over n elements of `data` (in place). */
+spc_status spc_epilogue_apply(const spc_epilogue* epi, float* data, size_t n, void* stream);
+
 /* ---- host-buffer drop-ins: copy in, run, copy out, synchronize ---- */
 spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters);

@@ -27,6 +27,10 @@ class spc_plan(C.Structure):
                                         "register_budget", "unroll_hint", "prefetch_hints")]
 
 
+class spc_epilogue(C.Structure):
+    _fields_ = [("alpha", C.c_float), ("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int)]
+
+
 class spc_counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("checked_vectors", "executed_vector_fmas",
                                            "output_vector_loads", "output_vector_stores")]
@@ -60,6 +64,13 @@ _SIGS = {
                                  C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p, C.c_void_p]),
     "spc_run_parallel": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
                                    C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p, C.c_void_p]),
+    "spc_sparse_fwd_ex": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
+                                    C.POINTER(spc_plan), C.c_int, C.POINTER(spc_epilogue), C.POINTER(spc_tensor),
+                                    C.c_void_p, C.c_void_p]),
+    "spc_sparse_bwi_ex": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
+                                    C.POINTER(spc_plan), C.c_int, C.POINTER(spc_epilogue), C.POINTER(spc_tensor),
+                                    C.c_void_p, C.c_void_p]),
+    "spc_epilogue_apply": (C.c_int, [C.POINTER(spc_epilogue), C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_run_parallel_host": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
                                         C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor),
                                         C.POINTER(spc_counters)]),

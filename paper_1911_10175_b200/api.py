@@ -397,6 +397,35 @@ def launch_count() -> int:
     return int(_lib.load().spc_launch_count())
 
 
+@dataclasses.dataclass
+class Epilogue:
+    """Fused FWD/BWI output epilogue (include/spconv_b200.h spc_epilogue):
+    v = acc*alpha (+ add); relu -> v > 0 ? v : 0; mask -> mask > 0 ? v : 0.
+    `add` / `mask` are device tensors with the output's ActNCHWc layout."""
+    alpha: float = 1.0
+    add: object = None
+    mask: object = None
+    relu: bool = False
+
+    def to_c(self) -> "_lib.spc_epilogue":
+        def ptr(t):
+            if t is None:
+                return None
+            if isinstance(t, BlockedTensor):
+                t = t.data
+            if not _is_torch_cuda(t):
+                raise SpconvError(_lib.SPC_ERR_ARG, "epilogue tensors must be CUDA tensors")
+            return t.data_ptr()
+        return _lib.spc_epilogue(float(self.alpha), ptr(self.add), ptr(self.mask), 1 if self.relu else 0)
+
+
+def epilogue_apply(epi: Epilogue, t) -> None:
+    """The epilogue as a standalone in-place pass over a device tensor."""
+    ce = epi.to_c()
+    _check(_lib.load().spc_epilogue_apply(C.byref(ce), C.c_void_p(t.data_ptr()), t.numel(),
+                                          C.c_void_p(_current_stream_ptr())))
+
+
 def _current_stream_ptr():
     import torch
     return torch.cuda.current_stream().cuda_stream
@@ -477,7 +506,7 @@ class PreparedPass:
     one C-ABI call on the given stream and no host synchronisation."""
 
     def __init__(self, a: BlockedTensor, b: BlockedTensor, shape: ConvShape, pl: KernelPlan,
-                 mode: RunMode = RunMode.sparse, out=None, counters=None):
+                 mode: RunMode = RunMode.sparse, out=None, counters=None, epilogue: Epilogue | None = None):
         import torch
         L = _lib.load()
         self.L = L
@@ -492,10 +521,19 @@ class PreparedPass:
         self._cd = spc_tensor(0, 0, 0, 0, 0, 0, 0, 0, 0, self.out.data_ptr(), numel)
         self._shape, self._plan = shape.to_c(), pl.to_c()
         self._mode = int(mode)
-        self._fn = {Component.fwd: L.spc_sparse_fwd, Component.bwi: L.spc_sparse_bwi,
-                    Component.bww: L.spc_sparse_bww}[Component(pl.comp)]
-        self._args = (C.byref(self._ca), C.byref(self._cb), C.byref(self._shape), C.byref(self._plan),
-                      self._mode, C.byref(self._cd))
+        if epilogue is not None and Component(pl.comp) == Component.bww:
+            raise SpconvError(_lib.SPC_ERR_ARG, "BWW has no output epilogue")
+        self._epi = epilogue.to_c() if epilogue is not None else None
+        self._epi_keep = epilogue  # keep add/mask tensors alive
+        if self._epi is None:
+            self._fn = {Component.fwd: L.spc_sparse_fwd, Component.bwi: L.spc_sparse_bwi,
+                        Component.bww: L.spc_sparse_bww}[Component(pl.comp)]
+            self._args = (C.byref(self._ca), C.byref(self._cb), C.byref(self._shape), C.byref(self._plan),
+                          self._mode, C.byref(self._cd))
+        else:
+            self._fn = {Component.fwd: L.spc_sparse_fwd_ex, Component.bwi: L.spc_sparse_bwi_ex}[Component(pl.comp)]
+            self._args = (C.byref(self._ca), C.byref(self._cb), C.byref(self._shape), C.byref(self._plan),
+                          self._mode, C.byref(self._epi), C.byref(self._cd))
         self._cnt_ptr = C.c_void_p(counters.data_ptr()) if counters is not None else C.c_void_p(None)
 
     def launch(self, stream_ptr: int) -> None:

@@ -316,9 +316,20 @@ static spc_status validate_bww(const spc_tensor* in, const spc_tensor* dy, const
     return check_act(in, SPC_LAYOUT_ACT_NCHWC, V, sh.N, sh.C, sh.H, sh.W, "bww input");
 }
 
+static Epi to_epi(const spc_epilogue* e) {
+    Epi d;
+    if (e) {
+        d.alpha = e->alpha;
+        d.add = e->add;
+        d.mask = e->mask;
+        d.relu = e->relu;
+    }
+    return d;
+}
+
 static spc_status run_fwd_bwi(bool fwd, const spc_tensor* src, const spc_tensor* filt, const spc_shape& sh,
                               const spc_plan& pl, int mode, spc_tensor* dst, spc_counters* d_counters,
-                              cudaStream_t st) {
+                              cudaStream_t st, const spc_epilogue* epi = nullptr) {
     spc_status s = fwd ? validate_fwd(src, filt, sh, pl) : validate_bwi(src, filt, sh, pl);
     if (s) return s;
     if (mode != SPC_SPARSE && mode != SPC_DENSE) return fail(SPC_ERR_ARG, "bad run mode");
@@ -327,7 +338,7 @@ static spc_status run_fwd_bwi(bool fwd, const spc_tensor* src, const spc_tensor*
     if ((s = start_counters(sh, pl, mode, d_counters, st))) return s;
     const DevShape ds = make_dev_shape(sh);
     cudaError_t e = launch_conv(fwd, mode == SPC_SPARSE, ds, pl.V, src->data, filt->data, dst->data,
-                                exec_slot(d_counters, mode), st);
+                                exec_slot(d_counters, mode), st, to_epi(epi));
     return e == cudaSuccess ? SPC_OK : cuda_fail(e, fwd ? "fwd launch" : "bwi launch");
 }
 
@@ -516,6 +527,39 @@ spc_status spc_sparse_bwi(const spc_tensor* grad_out, const spc_tensor* filt_t, 
                           const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
     return run_fwd_bwi(false, grad_out, filt_t, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
+}
+
+static spc_status check_epi(const spc_epilogue* epi) {
+    if (!epi) return fail(SPC_ERR_ARG, "null epilogue");
+    if (!(epi->alpha == epi->alpha)) return fail(SPC_ERR_ARG, "epilogue alpha is NaN");
+    return SPC_OK;
+}
+
+spc_status spc_sparse_fwd_ex(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
+                             const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
+                             spc_counters* d_counters, void* stream) {
+    if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    spc_status s = check_epi(epi);
+    if (s) return s;
+    return run_fwd_bwi(true, src, filt, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream, epi);
+}
+
+spc_status spc_sparse_bwi_ex(const spc_tensor* grad_out, const spc_tensor* filt_t, const spc_shape* shape,
+                             const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
+                             spc_counters* d_counters, void* stream) {
+    if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
+    spc_status s = check_epi(epi);
+    if (s) return s;
+    return run_fwd_bwi(false, grad_out, filt_t, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream, epi);
+}
+
+spc_status spc_epilogue_apply(const spc_epilogue* epi, float* data, size_t n, void* stream) {
+    spc_status s = check_epi(epi);
+    if (s) return s;
+    if (!data && n) return fail(SPC_ERR_ARG, "null data");
+    if ((s = check_device())) return s;
+    cudaError_t e = launch_epilogue(to_epi(epi), data, n, (cudaStream_t)stream);
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "epilogue");
 }
 
 spc_status spc_sparse_bww(const spc_tensor* input, const spc_tensor* grad_out, const spc_shape* shape,

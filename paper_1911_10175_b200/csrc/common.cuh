@@ -14,6 +14,24 @@ struct DevShape {
     int Hp, Wp;  // out_h(), out_w()  (P/include/spconv/tensor.hpp:44-45)
 };
 
+// Fused output epilogue of FWD/BWI: out = acc*alpha (+ add),
+// then ReLU (v > 0 ? v : 0, P/src/sparsity.cpp:13), then the ReLU-gradient
+// mask (mask > 0 ? v : 0, P/src/sparsity.cpp:26).  `add` and `mask` have
+// the output's ActNCHWc layout.  The identity epilogue leaves acc untouched.
+struct Epi {
+    float alpha = 1.0f;
+    const float* add = nullptr;
+    const float* mask = nullptr;
+    int relu = 0;
+    __host__ __device__ bool active() const { return alpha != 1.0f || add || mask || relu; }
+    __device__ __forceinline__ float apply(float v, size_t i) const {
+        v = add ? fmaf(v, alpha, add[i]) : v * alpha;
+        if (relu) v = v > 0.0f ? v : 0.0f;
+        if (mask) v = mask[i] > 0.0f ? v : 0.0f;
+        return v;
+    }
+};
+
 inline DevShape make_dev_shape(const spc_shape& s) {
     DevShape d;
     d.N = s.N; d.C = s.C; d.K = s.K; d.H = s.H; d.W = s.W; d.R = s.R; d.S = s.S;

@@ -8,13 +8,28 @@
 
 namespace spc {
 
+__global__ void epilogue_kernel(Epi epi, float* __restrict__ out, size_t n) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+        out[e] = epi.apply(out[e], e);
+}
+
+cudaError_t launch_epilogue(const Epi& epi, float* out, size_t n, cudaStream_t st) {
+    if (!epi.active() || n == 0) return cudaSuccess;
+    epilogue_kernel<<<148 * 8, 256, 0, st>>>(epi, out, n);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,
-                        float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+                        float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi) {
     // SPC_FORCE_GENERIC=1 selects the shape-general kernels (A/B testing only)
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
     if (!force_generic && tile_conv_supported(fwd, sh, V))
-        return launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st);
-    return launch_conv_generic(fwd, sparse, sh, V, src, filt, dst, exec_ctr, st);
+        return launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);  // fused epilogue
+    cudaError_t e = launch_conv_generic(fwd, sparse, sh, V, src, filt, dst, exec_ctr, st);
+    if (e != cudaSuccess) return e;
+    const size_t n = (size_t)sh.N * (fwd ? (size_t)sh.K * sh.Hp * sh.Wp : (size_t)sh.C * sh.H * sh.W);
+    return launch_epilogue(epi, dst, n, st);
 }
 
 cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V, const float* chk,

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                                                                    float* __restrict__ dst,
                                                                    unsigned long long* __restrict__ exec_ctr,
                                                                    const int* __restrict__ sel, int want,
-                                                                   int group_fastest) {
+                                                                   int group_fastest, Epi epi) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     // device-side kernel choice (see launch_tile_conv): the variant whose
     // selector value does not match exits before touching memory
@@ -462,7 +462,12 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                 }
                 else o.v[j] = acc[ty * TW + tx][j];
             }
-            o.store(dst + ((((size_t)i * CoB + k0 / 16) * Ho + y) * Wo + x) * 16 + (k0 % 16));
+            const size_t off = ((((size_t)i * CoB + k0 / 16) * Ho + y) * Wo + x) * 16 + (k0 % 16);
+            if (epi.active()) {
+#pragma unroll
+                for (int j = 0; j < KK; ++j) o.v[j] = epi.apply(o.v[j], off + j);
+            }
+            o.store(dst + off);
         }
     }
     if (SPARSE && exec_ctr) {
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF = 1, int JT = 0>
 static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
                               unsigned long long* exec_ctr, cudaStream_t st, const int* sel = nullptr,
-                              int want = 0) {
+                              int want = 0, const Epi& epi = Epi{}) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     const int Co = FWD ? sh.K : sh.C;
     const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
@@ -499,7 +504,7 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
     const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
     const size_t src_bytes = (size_t)sh.N * Ci * Hs * Ws * sizeof(float);
     const int group_fastest = src_bytes > ((size_t)48 << 20) ? 1 : 0;
-    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest);
+    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest, epi);
     note_launch();
     return cudaGetLastError();
 }
@@ -657,11 +662,11 @@ bool tile_conv_supported(bool fwd, const DevShape& sh, int V) {
 #endif
 
 cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
-                             float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+                             float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi) {
     const int Co = fwd ? sh.K : sh.C;
     const bool kk4 = Co % 128 == 0;
 #define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
-    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st)
+    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st, nullptr, 0, epi)
     if (sh.R == 3 && sh.O == 1) {
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
@@ -674,11 +679,11 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
             if (e != cudaSuccess) return e;
             launch_density_probe(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel, st);
-            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0)
-                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0);
+            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi)
+                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi);
             if (e == cudaSuccess)
-                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1)
-                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1);
+                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi)
+                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi);
             cudaFreeAsync(sel, st);
             return e;
         }
