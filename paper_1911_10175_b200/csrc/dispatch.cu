@@ -3,6 +3,7 @@
 
 #include <cstdlib>
 
+#include "pw_conv.h"
 #include "tile_bww.h"
 #include "tile_conv.h"
 
@@ -24,6 +25,19 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
                         float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi) {
     // SPC_FORCE_GENERIC=1 selects the shape-general kernels (A/B testing only)
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
+    // SPC_PW_OFF=1 routes 1x1 convs to the tile kernel (A/B testing only)
+    static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
+    if (!force_generic && !pw_off && pw_conv_supported(fwd, sh, V)) {
+        int* finite = nullptr;
+        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        launch_filter_finite(filt, (size_t)sh.K * sh.C, finite, st);
+        e = launch_pw_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
+        // filters with Inf/NaN: the per-element-skip tile kernel (exits otherwise)
+        if (e == cudaSuccess) e = launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, finite, 0);
+        cudaFreeAsync(finite, st);
+        return e;
+    }
     if (!force_generic && tile_conv_supported(fwd, sh, V))
         return launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);  // fused epilogue
     cudaError_t e = launch_conv_generic(fwd, sparse, sh, V, src, filt, dst, exec_ctr, st);

@@ -662,11 +662,12 @@ bool tile_conv_supported(bool fwd, const DevShape& sh, int V) {
 #endif
 
 cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
-                             float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi) {
+                             float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi,
+                             const int* xsel, int xwant) {
     const int Co = fwd ? sh.K : sh.C;
     const bool kk4 = Co % 128 == 0;
 #define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
-    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st, nullptr, 0, epi)
+    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st, xsel, xwant, epi)
     if (sh.R == 3 && sh.O == 1) {
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
