@@ -466,3 +466,41 @@ def test_baseline_layers_match_reference_cpu(sp, cfg, idx):
         assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
         assert res.counters.checked_vectors == ref_cnt["checked_vectors"]
         r.close()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("comp", [0, 1])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_pointwise_nonfinite_filter_keeps_skip_semantics(sp, comp, stride):
+    """The 1x1 kernel executes zero products (exact for finite filters); a filter
+    with Inf/NaN must still follow the reference's skip semantics (0 inputs are
+    skipped, so 0*Inf never happens): GPU == reference CPU incl. NaN/Inf positions."""
+    V = 16
+    sh = sp.ConvShape.make(3, 64, 128, 9, 10, 1, 1, stride, stride)
+    rng = np.random.default_rng(11 + comp + stride)
+    hp, wp = sh.out_h(), sh.out_w()
+    G = rng.standard_normal((sh.K, sh.C, 1, 1)).astype(np.float32)
+    if comp == 0:
+        X = np.maximum(rng.standard_normal((sh.N, sh.C, sh.H, sh.W)), 0).astype(np.float32)
+        X[:, 5] = 0.0       # channel 5 all zero: its Inf/NaN weights must be skipped
+        X[:, 9, 0, 0] = 3.0  # channel 9 has one nonzero: Inf propagates there only
+        G[7, 5, 0, 0], G[100, 5, 0, 0], G[3, 9, 0, 0] = np.inf, np.nan, np.inf
+        a, b = X, G
+    else:
+        X = np.maximum(rng.standard_normal((sh.N, sh.K, hp, wp)), 0).astype(np.float32)
+        X[:, 40] = 0.0
+        G[40, 7, 0, 0], G[40, 60, 0, 0] = np.inf, -np.inf
+        a, b = X, G
+    r = O.RefRun(comp, 0, sh.astuple(), V, a, b)
+    r.exec(0, 4)
+    ref_out, ref_cnt, _ = r.result()
+    pl = sp.plan(sh, sp.Component(comp), V)
+    ta = sp.pack_act_nchwc(a, V)
+    tb = sp.pack_filter(b, V, swap_kc=(comp == 1))
+    res = sp.run_parallel(ta, tb, sh, pl, sp.RunMode.sparse)
+    got = sp.unpack(res.out)
+    assert np.array_equal(np.isnan(got), np.isnan(ref_out))
+    assert np.array_equal(np.isinf(got), np.isinf(ref_out))
+    fin = np.isfinite(ref_out)
+    assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
+    assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
