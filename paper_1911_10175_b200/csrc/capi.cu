@@ -9,6 +9,7 @@
 //   per-entry C,K % V checks  P/src/kernels.cpp:172-173, 208-209, 244-245
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <mutex>
@@ -621,6 +622,8 @@ spc_status host_streams(HostStreams*& hs) {
 }
 }  // namespace
 
+static constexpr int kMaxHostChunks = 64;
+
 spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters) {
     if (!a || !b || !shape || !plan || !dst) return fail(SPC_ERR_ARG, "null argument");
@@ -648,8 +651,17 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     const spc_tensor* oth = bww ? (on_input ? b : a) : nullptr;
     const size_t io_bytes = (a->numel + b->numel + out.numel) * sizeof(float);
     const int units = bww ? (shape->N + V - 1) / V : shape->N;  // chunk granularity
-    int nc = io_bytes >= (size_t)64 << 20 ? (io_bytes >= (size_t)512 << 20 ? 8 : 4) : 1;
+    // chunk count: ~chunk_mb of traffic per chunk, at most max_chunks (the
+    // H2D / kernel / D2H of consecutive chunks overlap on 3 streams; the
+    // call's exposed tail is one chunk's kernel + D2H)
+    static const int chunk_mb = std::getenv("SPC_HOST_CHUNK_MB") ? std::atoi(std::getenv("SPC_HOST_CHUNK_MB")) : 48;
+    static const int max_chunks =
+        std::getenv("SPC_HOST_MAX_CHUNKS") ? std::atoi(std::getenv("SPC_HOST_MAX_CHUNKS")) : 16;
+    int nc = (int)((io_bytes + ((size_t)chunk_mb << 20) - 1) / ((size_t)chunk_mb << 20));
+    if (nc > max_chunks) nc = max_chunks;
+    if (nc > kMaxHostChunks) nc = kMaxHostChunks;
     if (nc > units) nc = units;
+    if (nc < 1) nc = 1;
 
     float *da = nullptr, *db = nullptr, *dd = nullptr, *dpart = nullptr;
     spc_counters* dc = nullptr;
@@ -729,7 +741,7 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
         }
         cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0);
     }
-    spc_counters hc[8];
+    spc_counters hc[kMaxHostChunks];
     if (st == SPC_OK && counters) {
         for (int c = 0; c < nc; ++c)
             cudaMemcpyAsync(&hc[c], dc + c, sizeof(spc_counters), cudaMemcpyDeviceToHost, hs->s[c % 3]);

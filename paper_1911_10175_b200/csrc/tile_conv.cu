@@ -189,7 +189,8 @@ __device__ __forceinline__ void jt_words(Acc& acc, const Gv& g, const float* vv,
 // table when the previous block's measured density (nonzeros / region
 // pixels, summed over the CTA's warps) is at most JT%, else per-pixel
 // branches.  All variants accumulate in the same order (bitwise identical).
-template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF, int JT, bool SPARSE>
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF, int JT, bool SPARSE,
+          bool EPI>
 __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, const float* __restrict__ src,
                                                                    const float* __restrict__ filt,
                                                                    float* __restrict__ dst,
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                 else o.v[j] = acc[ty * TW + tx][j];
             }
             const size_t off = ((((size_t)i * CoB + k0 / 16) * Ho + y) * Wo + x) * 16 + (k0 % 16);
-            if (epi.active()) {
+            if constexpr (EPI) {  // a separate instantiation: the unrolled epilogue costs registers and I-cache
 #pragma unroll
                 for (int j = 0; j < KK; ++j) o.v[j] = epi.apply(o.v[j], off + j);
             }
@@ -480,7 +481,8 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 }
 
 // ---------------------------------------------------------------- dispatch
-template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF = 1, int JT = 0>
+template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF = 1, int JT = 0,
+          bool WITH_EPI = false>
 static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
                               unsigned long long* exec_ctr, cudaStream_t st, const int* sel = nullptr,
                               int want = 0, const Epi& epi = Epi{}) {
@@ -490,15 +492,23 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
     const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
     const int tiles_y = (Ho + TH * NWY - 1) / (TH * NWY);
     dim3 grid(tiles_x * tiles_y * (Co / (32 * KK)), sh.N, 1);
-    auto kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true>
-                       : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
+    using KFn = void (*)(DevShape, const float*, const float*, float*, unsigned long long*, const int*, int, int, Epi);
+    KFn kern;
+    const bool with_epi = epi.active();
+    if (with_epi) {
+        if constexpr (WITH_EPI)
+            kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, true>
+                          : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, true>;
+        else
+            return cudaErrorInvalidValue;
+    } else {
+        kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, false>
+                      : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, false>;
+    }
+    static bool attr_set[2][2] = {{false, false}, {false, false}};  // per instantiation: [epi][sparse]
+    if (!attr_set[with_epi][sparse]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
-        auto kern2 = !sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true>
-                             : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false>;
-        cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
-        attr_set = true;
+        attr_set[with_epi][sparse] = true;
     }
     const int Ci = FWD ? sh.C : sh.K;
     const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
@@ -667,7 +677,7 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
     const int Co = fwd ? sh.K : sh.C;
     const bool kk4 = Co % 128 == 0;
 #define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
-    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR>(sparse, sh, src, filt, dst, exec_ctr, st, xsel, xwant, epi)
+    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, xsel, xwant, epi)
     if (sh.R == 3 && sh.O == 1) {
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
@@ -680,11 +690,11 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
             if (e != cudaSuccess) return e;
             launch_density_probe(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel, st);
-            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi)
-                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi);
+            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi)
+                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi);
             if (e == cudaSuccess)
-                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi)
-                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi);
+                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi)
+                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi);
             cudaFreeAsync(sel, st);
             return e;
         }
