@@ -32,6 +32,54 @@ struct Epi {
     }
 };
 
+// Copy/compute overlap inside ONE launch (the host-buffer path): the CTAs of
+// image i wait for the ready word of i's input chunk, which the copy-in
+// stream raises (stream memory op) right after that chunk's H2D; the last CTA
+// to finish a chunk raises its out_ready word, on which the copy-out stream
+// waits before that chunk's D2H.  Disabled when in_ready == nullptr.  Waits
+// are bounded (a stuck copy sets *err instead of hanging the GPU).
+struct Gate {
+    const unsigned* in_ready = nullptr;
+    unsigned* done = nullptr;       // finished CTAs per chunk
+    unsigned* out_ready = nullptr;  // 1 once all of a chunk's outputs are written
+    unsigned* err = nullptr;
+    int ipc = 1;                    // images per chunk
+    int nimg = 0;                   // images in the launch
+
+    __device__ __forceinline__ void wait_input(int image) const {
+        if (in_ready == nullptr) return;
+        if (threadIdx.x == 0) {
+            const unsigned* w = in_ready + image / ipc;
+            for (unsigned n = 0;; ++n) {
+                unsigned v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+                if (v) break;
+                if ((n & 1023u) == 0 && *(volatile const unsigned*)err) break;  // another CTA gave up
+                if (n > (1u << 24)) {  // ~seconds: give up, report
+                    atomicExch(err, 1u);
+                    break;
+                }
+                __nanosleep(200);
+            }
+        }
+        __syncthreads();
+    }
+    __device__ __forceinline__ void finish(int image) const {
+        if (done == nullptr) return;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int c = image / ipc;
+            const int in_chunk = (nimg - c * ipc) < ipc ? (nimg - c * ipc) : ipc;
+            const unsigned expected = gridDim.x * (unsigned)in_chunk;
+            if (atomicAdd(done + c, 1u) + 1u == expected) {
+                __threadfence_system();  // out_ready is mapped host memory the host thread polls
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(out_ready + c), "r"(1u) : "memory");
+            }
+        }
+    }
+};
+
 inline DevShape make_dev_shape(const spc_shape& s) {
     DevShape d;
     d.N = s.N; d.C = s.C; d.K = s.K; d.H = s.H; d.W = s.W; d.R = s.R; d.S = s.S;

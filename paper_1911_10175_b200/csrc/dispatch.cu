@@ -21,8 +21,13 @@ cudaError_t launch_epilogue(const Epi& epi, float* out, size_t n, cudaStream_t s
     return cudaGetLastError();
 }
 
+bool conv_supports_gate(bool fwd, const DevShape& sh, int V) {
+    static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
+    return !force_generic && (pw_conv_supported(fwd, sh, V) || tile_conv_supported(fwd, sh, V));
+}
+
 cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,
-                        float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi) {
+                        float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi, const Gate& gate) {
     // SPC_FORCE_GENERIC=1 selects the shape-general kernels (A/B testing only)
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
     // SPC_PW_OFF=1 routes 1x1 convs to the tile kernel (A/B testing only)
@@ -32,14 +37,14 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
         cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
         if (e != cudaSuccess) return e;
         launch_filter_finite(filt, (size_t)sh.K * sh.C, finite, st);
-        e = launch_pw_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
+        e = launch_pw_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
         // filters with Inf/NaN: the per-element-skip tile kernel (exits otherwise)
-        if (e == cudaSuccess) e = launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, finite, 0);
+        if (e == cudaSuccess) e = launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, finite, 0, gate);
         cudaFreeAsync(finite, st);
         return e;
     }
     if (!force_generic && tile_conv_supported(fwd, sh, V))
-        return launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);  // fused epilogue
+        return launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nullptr, 0, gate);
     cudaError_t e = launch_conv_generic(fwd, sparse, sh, V, src, filt, dst, exec_ctr, st);
     if (e != cudaSuccess) return e;
     const size_t n = (size_t)sh.N * (fwd ? (size_t)sh.K * sh.Hp * sh.Wp : (size_t)sh.C * sh.H * sh.W);

@@ -10,7 +10,10 @@ namespace spc {
 // FWD (fwd=true) or BWI: picks the tuned V=16 tile kernel when the geometry
 // has one, else the shape-general kernel.
 cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,
-                        float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi = Epi{});
+                        float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi = Epi{},
+                        const Gate& gate = Gate{});
+// True when launch_conv runs a kernel that honours a Gate (tile / 1x1 paths).
+bool conv_supports_gate(bool fwd, const DevShape& sh, int V);
 
 // Standalone epilogue over n output elements (the generic kernels' path).
 cudaError_t launch_epilogue(const Epi& epi, float* out, size_t n, cudaStream_t st);

@@ -79,10 +79,11 @@ template <bool FWD, int KK, int NWK, int STR, bool COUNT>
 __global__ void __launch_bounds__(NWK * 32) pw_conv_kernel(DevShape sh, const float* __restrict__ src,
                                                            const float* __restrict__ filt, float* __restrict__ dst,
                                                            unsigned long long* __restrict__ exec_ctr,
-                                                           const int* __restrict__ finite, Epi epi) {
+                                                           const int* __restrict__ finite, Epi epi, Gate gate) {
     // a filter with Inf/NaN runs the per-element-skip tile kernel instead
     // (launched alongside with the same flag, want = 0)
     if (finite != nullptr && __ldg(finite) == 0) return;
+    gate.wait_input(blockIdx.y);
     constexpr int NT = NWK * 32;
     __shared__ __align__(16) float Xs[PW_NST][PW_P * PW_PS];
 
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(NWK * 32) pw_conv_kernel(DevShape sh, const fl
         const uint32_t total = __reduce_add_sync(0xffffffffu, nzcount);
         if (lane == 0 && total) atomicAdd(exec_ctr, (unsigned long long)total * (2 * KK));
     }
+    gate.finish(blockIdx.y);
 }
 
 // flag = 1 when every filter element is finite (zero-quad skipping is then
@@ -226,27 +228,27 @@ __global__ void __launch_bounds__(256) filter_finite_kernel(const float* __restr
 
 template <bool FWD, int KK, int NWK, int STR>
 cudaError_t pw_launch(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
-                      unsigned long long* exec_ctr, cudaStream_t st, const int* finite, const Epi& epi) {
+                      unsigned long long* exec_ctr, cudaStream_t st, const int* finite, const Epi& epi, const Gate& gate) {
     const int Co = FWD ? sh.K : sh.C;
     const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
     const int ntile = (Ho * Wo + PW_P - 1) / PW_P;
     dim3 grid(ntile * (Co / (32 * KK * NWK)), sh.N, 1);
     if (sparse)
-        pw_conv_kernel<FWD, KK, NWK, STR, true><<<grid, NWK * 32, 0, st>>>(sh, src, filt, dst, exec_ctr, finite, epi);
+        pw_conv_kernel<FWD, KK, NWK, STR, true><<<grid, NWK * 32, 0, st>>>(sh, src, filt, dst, exec_ctr, finite, epi, gate);
     else
-        pw_conv_kernel<FWD, KK, NWK, STR, false><<<grid, NWK * 32, 0, st>>>(sh, src, filt, dst, exec_ctr, finite, epi);
+        pw_conv_kernel<FWD, KK, NWK, STR, false><<<grid, NWK * 32, 0, st>>>(sh, src, filt, dst, exec_ctr, finite, epi, gate);
     note_launch();
     return cudaGetLastError();
 }
 
 template <bool FWD, int STR>
 cudaError_t pw_pick(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
-                    unsigned long long* exec_ctr, cudaStream_t st, const int* finite, const Epi& epi) {
+                    unsigned long long* exec_ctr, cudaStream_t st, const int* finite, const Epi& epi, const Gate& gate) {
     const int Co = FWD ? sh.K : sh.C;
-    if (Co % 512 == 0) return pw_launch<FWD, 4, 4, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
-    if (Co % 256 == 0) return pw_launch<FWD, 4, 2, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
-    if (Co % 128 == 0) return pw_launch<FWD, 4, 1, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
-    return pw_launch<FWD, 2, 1, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
+    if (Co % 512 == 0) return pw_launch<FWD, 4, 4, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
+    if (Co % 256 == 0) return pw_launch<FWD, 4, 2, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
+    if (Co % 128 == 0) return pw_launch<FWD, 4, 1, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
+    return pw_launch<FWD, 2, 1, STR>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
 }
 
 }  // namespace
@@ -260,11 +262,11 @@ bool pw_conv_supported(bool fwd, const DevShape& sh, int V) {
 
 cudaError_t launch_pw_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
                            float* dst, unsigned long long* exec_ctr, cudaStream_t st, const int* finite,
-                           const Epi& epi) {
-    if (fwd) return sh.O == 1 ? pw_pick<true, 1>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi)
-                              : pw_pick<true, 2>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
-    return sh.O == 1 ? pw_pick<false, 1>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi)
-                     : pw_pick<false, 2>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi);
+                           const Epi& epi, const Gate& gate) {
+    if (fwd) return sh.O == 1 ? pw_pick<true, 1>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate)
+                              : pw_pick<true, 2>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
+    return sh.O == 1 ? pw_pick<false, 1>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate)
+                     : pw_pick<false, 2>(sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
 }
 
 void launch_filter_finite(const float* filt, size_t n, int* flag, cudaStream_t st) {

@@ -8,6 +8,6 @@ bool pw_conv_supported(bool fwd, const DevShape& sh, int V);
 // exact), 0 = per-element tests; written by launch_filter_finite.
 cudaError_t launch_pw_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
                            float* dst, unsigned long long* exec_ctr, cudaStream_t st, const int* finite,
-                           const Epi& epi = Epi{});
+                           const Epi& epi = Epi{}, const Gate& gate = Gate{});
 void launch_filter_finite(const float* filt, size_t n, int* flag, cudaStream_t st);
 }  // namespace spc

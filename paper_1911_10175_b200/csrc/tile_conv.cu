@@ -196,11 +196,12 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                                                                    float* __restrict__ dst,
                                                                    unsigned long long* __restrict__ exec_ctr,
                                                                    const int* __restrict__ sel, int want,
-                                                                   int group_fastest, Epi epi) {
+                                                                   int group_fastest, Epi epi, Gate gate) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     // device-side kernel choice (see launch_tile_conv): the variant whose
     // selector value does not match exits before touching memory
     if (sel != nullptr && __ldg(sel) != want) return;
+    gate.wait_input(blockIdx.y);
     using AY = typename Gm::AY;
     using AX = typename Gm::AX;
     constexpr int RH = Gm::RH, RWW = Gm::RWW, NQ = Gm::NQ, ROW = Gm::ROW;
@@ -478,6 +479,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
         if (lane == 0 && total) atomicAdd(exec_ctr, (unsigned long long)total * (2 * KK));
     }
+    gate.finish(blockIdx.y);
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -485,14 +487,15 @@ template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int 
           bool WITH_EPI = false>
 static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src, const float* filt, float* dst,
                               unsigned long long* exec_ctr, cudaStream_t st, const int* sel = nullptr,
-                              int want = 0, const Epi& epi = Epi{}) {
+                              int want = 0, const Epi& epi = Epi{}, const Gate& gate = Gate{}) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     const int Co = FWD ? sh.K : sh.C;
     const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
     const int tiles_x = (Wo + TW * NWX - 1) / (TW * NWX);
     const int tiles_y = (Ho + TH * NWY - 1) / (TH * NWY);
     dim3 grid(tiles_x * tiles_y * (Co / (32 * KK)), sh.N, 1);
-    using KFn = void (*)(DevShape, const float*, const float*, float*, unsigned long long*, const int*, int, int, Epi);
+    using KFn = void (*)(DevShape, const float*, const float*, float*, unsigned long long*, const int*, int, int, Epi,
+                         Gate);
     KFn kern;
     const bool with_epi = epi.active();
     if (with_epi) {
@@ -514,7 +517,7 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
     const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
     const size_t src_bytes = (size_t)sh.N * Ci * Hs * Ws * sizeof(float);
     const int group_fastest = src_bytes > ((size_t)48 << 20) ? 1 : 0;
-    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest, epi);
+    kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest, epi, gate);
     note_launch();
     return cudaGetLastError();
 }
@@ -618,7 +621,8 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
 // the whole tensor).  sel = 1 when density <= pct% (the jump-table kernel
 // wins), else 0.
 __global__ void __launch_bounds__(256) density_probe_kernel(const float* __restrict__ t, size_t n, int pct,
-                                                            int* __restrict__ sel) {
+                                                            int* __restrict__ sel, Gate gate) {
+    gate.wait_input(0);  // gated launches sample the first input chunk once it has landed
     __shared__ unsigned long long cnt[2];
     if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -648,11 +652,13 @@ __global__ void __launch_bounds__(256) density_probe_kernel(const float* __restr
     }
 }
 
-void launch_density_probe(const float* t, size_t n, int pct, int* sel, cudaStream_t st) {
+void launch_density_probe(const float* t, size_t n, int pct, int* sel, cudaStream_t st, const Gate& gate) {
     // SPC_JT_PCT overrides the jump-table density threshold (0 = never, 100 = always)
     static const int override_pct = std::getenv("SPC_JT_PCT") ? std::atoi(std::getenv("SPC_JT_PCT")) : -1;
     if (override_pct >= 0) pct = override_pct;
-    density_probe_kernel<<<1, 256, 0, st>>>(t, n, pct, sel);
+    Gate g = gate;
+    g.done = nullptr;  // the probe only waits; it never completes a chunk
+    density_probe_kernel<<<1, 256, 0, st>>>(t, n, pct, sel, g);
     note_launch();
 }
 
@@ -673,11 +679,11 @@ bool tile_conv_supported(bool fwd, const DevShape& sh, int V) {
 
 cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
                              float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi,
-                             const int* xsel, int xwant) {
+                             const int* xsel, int xwant, const Gate& gate) {
     const int Co = fwd ? sh.K : sh.C;
     const bool kk4 = Co % 128 == 0;
 #define SPC_L(F, KK, TH, TW, NWY, NWX, R, STR) \
-    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, xsel, xwant, epi)
+    return launch_cfg<F, KK, TH, TW, NWY, NWX, R, R, STR, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, xsel, xwant, epi, gate)
     if (sh.R == 3 && sh.O == 1) {
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
@@ -689,12 +695,14 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             int* sel = nullptr;
             cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
             if (e != cudaSuccess) return e;
-            launch_density_probe(src, (size_t)sh.N * Ci * Hs * Ws, 15, sel, st);
-            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi)
-                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi);
+            // gated (host-buffer) launches sample only the first input chunk
+            const size_t per_img = (size_t)Ci * Hs * Ws;
+            launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 15, sel, st, gate);
+            e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate)
+                    : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate);
             if (e == cudaSuccess)
-                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi)
-                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi);
+                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
+                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
             cudaFreeAsync(sel, st);
             return e;
         }

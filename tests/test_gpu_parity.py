@@ -504,3 +504,34 @@ def test_pointwise_nonfinite_filter_keeps_skip_semantics(sp, comp, stride):
     fin = np.isfinite(ref_out)
     assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
     assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
+
+
+def test_gated_host_path_equals_device_path(tmp_path):
+    """SPC_HOST_GATE=1: FWD/BWI host-buffer calls as one launch whose CTAs wait
+    for their input chunk (Gate, common.cuh) -- bitwise equal to the device call."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, paper_1911_10175_b200 as sp
+from paper_1911_10175_b200 import workloads as wl
+V = 16
+for dims in [(12, 64, 128, 20, 22, 3, 1), (9, 128, 128, 15, 14, 3, 1), (7, 64, 256, 14, 14, 1, 1), (5, 64, 128, 14, 14, 1, 2)]:
+    N, C, K, H, W, R, O = dims
+    sh = sp.ConvShape.make(N, C, K, H, W, R, R, O, O)
+    rng = np.random.default_rng(N)
+    G = rng.standard_normal((K, C, R, R)).astype(np.float32)
+    for comp in (sp.Component.fwd, sp.Component.bwi):
+        shp = (N, C, H, W) if comp == sp.Component.fwd else (N, K, sh.out_h(), sh.out_w())
+        x = np.maximum(rng.standard_normal(shp) - 0.3, 0).astype(np.float32)
+        a, b = sp.pack_act_nchwc(x, V), sp.pack_filter(G, V, comp == sp.Component.bwi)
+        pl = sp.plan(sh, comp, V)
+        host = sp.run_parallel(a, b, sh, pl, sp.RunMode.sparse)
+        dev = sp.run_parallel(a.to("cuda"), b.to("cuda"), sh, pl, sp.RunMode.sparse)
+        assert np.array_equal(host.out.data, dev.out.data.cpu().numpy()), (dims, comp)
+        assert host.counters == dev.counters
+print("ok")
+'''
+    env = dict(os.environ, SPC_HOST_GATE="1", SPC_HOST_CHUNK_MB="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
