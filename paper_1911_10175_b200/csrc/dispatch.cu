@@ -3,6 +3,7 @@
 
 #include <cstdlib>
 
+#include "pw_bww.h"
 #include "pw_conv.h"
 #include "tile_bww.h"
 #include "tile_conv.h"
@@ -54,6 +55,16 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
 cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V, const float* chk,
                        const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
+    static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
+    if (!force_generic && !pw_off && pw_bww_supported(check_input, sh, V)) {
+        int* finite = nullptr;
+        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        launch_finite_all(oth, (size_t)sh.N * sh.K * sh.Hp * sh.Wp, finite, st);  // dY (ActNCHWc)
+        e = launch_pw_bww(sparse, sh, chk, oth, dst, exec_ctr, finite, st);
+        cudaFreeAsync(finite, st);
+        return e;
+    }
     if (!force_generic && tile_bww_supported(check_input, sh, V))
         return launch_tile_bww(check_input, sparse, sh, chk, oth, dst, exec_ctr, st);
     const int splits = bww_generic_splits(sh);

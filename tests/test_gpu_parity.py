@@ -535,3 +535,31 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("stride", [1, 2])
+def test_pointwise_bww_nonfinite_grad_keeps_skip_semantics(sp, stride):
+    """1x1 BWW (check = input) executes zero products for finite dY; a dY with
+    Inf/NaN must follow the reference's skip semantics (GPU == reference CPU)."""
+    V = 16
+    sh = sp.ConvShape.make(19, 64, 128, 9, 10, 1, 1, stride, stride)
+    rng = np.random.default_rng(5 + stride)
+    hp, wp = sh.out_h(), sh.out_w()
+    D = np.maximum(rng.standard_normal((sh.N, sh.C, sh.H, sh.W)), 0).astype(np.float32)
+    dY = rng.standard_normal((sh.N, sh.K, hp, wp)).astype(np.float32)
+    D[:, 3] = 0.0                      # channel 3 all zero: dY's Inf/NaN must not reach dG[:, 3]
+    dY[2, 7, 1, 1], dY[5, 90, 0, 2] = np.inf, np.nan
+    for finite in (True, False):
+        y = np.nan_to_num(dY, nan=0.0, posinf=0.0) if finite else dY
+        r = O.RefRun(2, 0, sh.astuple(), V, D, y)
+        r.exec(0, 4)
+        ref_out, ref_cnt, _ = r.result()
+        pl = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck.input)
+        res = sp.run_parallel(sp.pack_act_chwnn(D, V), sp.pack_act_nchwc(y, V), sh, pl, sp.RunMode.sparse)
+        got = sp.unpack(res.out)
+        assert np.array_equal(np.isnan(got), np.isnan(ref_out)), finite
+        assert np.array_equal(np.isinf(got), np.isinf(ref_out)), finite
+        fin = np.isfinite(ref_out)
+        assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
+        assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
