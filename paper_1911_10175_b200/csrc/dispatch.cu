@@ -5,6 +5,7 @@
 
 #include "pw_bww.h"
 #include "pw_conv.h"
+#include "pw_gemm.h"
 #include "tile_bww.h"
 #include "tile_conv.h"
 
@@ -22,9 +23,17 @@ cudaError_t launch_epilogue(const Epi& epi, float* out, size_t n, cudaStream_t s
     return cudaGetLastError();
 }
 
+// SPC_PW_GEMM=0 routes 1x1 FWD/BWI to the lane-per-channel pw_conv kernel (A/B testing)
+static bool use_pw_gemm() {
+    static const bool off = std::getenv("SPC_PW_GEMM") && std::atoi(std::getenv("SPC_PW_GEMM")) == 0;
+    return !off;
+}
+
 bool conv_supports_gate(bool fwd, const DevShape& sh, int V) {
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
-    return !force_generic && (pw_conv_supported(fwd, sh, V) || tile_conv_supported(fwd, sh, V));
+    if (force_generic) return false;
+    if (use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) return false;  // the GEMM kernel has no Gate
+    return pw_conv_supported(fwd, sh, V) || tile_conv_supported(fwd, sh, V);
 }
 
 cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,
@@ -33,6 +42,15 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
     // SPC_PW_OFF=1 routes 1x1 convs to the tile kernel (A/B testing only)
     static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
+    if (!force_generic && !pw_off && use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) {
+        int* finite = nullptr;
+        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        launch_finite_all(filt, (size_t)sh.K * sh.C, finite, st);
+        e = launch_pw_gemm(fwd, sparse, sh, src, filt, dst, exec_ctr, finite, st, epi);
+        cudaFreeAsync(finite, st);
+        return e;
+    }
     if (!force_generic && !pw_off && pw_conv_supported(fwd, sh, V)) {
         int* finite = nullptr;
         cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
