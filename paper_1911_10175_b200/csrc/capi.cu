@@ -373,6 +373,34 @@ __global__ void relu_grad_mask_kernel(const float* __restrict__ pre, const float
         out[e] = pre[e] > 0.0f ? up[e] : 0.0f;  // P/src/sparsity.cpp:26: zero where !(pre > 0)
 }
 
+// V = 16 fast path: a CTA transposes one (16-image block, 16-channel block,
+// 16-pixel run) tile through shared memory: 16 images x 16 px x 16 ch read as
+// contiguous 1 KB runs per image, written as contiguous 1 KB runs per channel.
+__global__ void __launch_bounds__(256) nchwc_to_chwnn16_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                                               int n, int c, int hw) {
+    __shared__ float t[16][16][17];  // [image][pixel][channel] (+1 pad)
+    const int cb = blockIdx.y, nb = blockIdx.z, CB = c / 16;
+    const int p0 = blockIdx.x * 16;
+    // load: 16 images x 16 px x 4 float4
+    for (int e = threadIdx.x; e < 16 * 16 * 4; e += 256) {
+        const int q = e & 3, p = (e >> 2) & 15, i = e >> 6;
+        const int img = nb * 16 + i, px = p0 + p;
+        float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (img < n && px < hw) v = __ldg(reinterpret_cast<const float4*>(src + (((size_t)img * CB + cb) * hw + px) * 16) + q);
+        t[i][p][q * 4 + 0] = v.x; t[i][p][q * 4 + 1] = v.y; t[i][p][q * 4 + 2] = v.z; t[i][p][q * 4 + 3] = v.w;
+    }
+    __syncthreads();
+    // store: 16 channels x 16 px x 4 float4 (lanes = images)
+    for (int e = threadIdx.x; e < 16 * 16 * 4; e += 256) {
+        const int q = e & 3, p = (e >> 2) & 15, ch = e >> 6;
+        const int px = p0 + p;
+        if (px < hw) {
+            const float4 v = make_float4(t[q * 4 + 0][p][ch], t[q * 4 + 1][p][ch], t[q * 4 + 2][p][ch], t[q * 4 + 3][p][ch]);
+            *(reinterpret_cast<float4*>(dst + (((size_t)nb * c + cb * 16 + ch) * hw + px) * 16) + q) = v;
+        }
+    }
+}
+
 // ActNCHWc -> ActCHWNn with zero-filled ragged tail lanes (P/src/tensor.cpp:94-108).
 __global__ void nchwc_to_chwnn_kernel(const float* __restrict__ src, float* __restrict__ dst, int n, int c,
                                       int h, int w, int V) {
@@ -992,8 +1020,14 @@ spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stre
     dst->n = src->n; dst->c = src->c; dst->h = src->h; dst->w = src->w;
     dst->k = dst->r = dst->s = 0;
     dst->numel = need;
-    nchwc_to_chwnn_kernel<<<grid_for(need), 256, 0, (cudaStream_t)stream>>>(src->data, dst->data, src->n, src->c,
-                                                                           src->h, src->w, V);
+    if (V == 16) {
+        const int hw = src->h * src->w;
+        dim3 grid((hw + 15) / 16, src->c / 16, (src->n + 15) / 16);
+        nchwc_to_chwnn16_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src->data, dst->data, src->n, src->c, hw);
+    } else {
+        nchwc_to_chwnn_kernel<<<grid_for(need), 256, 0, (cudaStream_t)stream>>>(src->data, dst->data, src->n,
+                                                                               src->c, src->h, src->w, V);
+    }
     note_launch();
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SPC_OK : cuda_fail(e, "nchwc_to_chwnn");
