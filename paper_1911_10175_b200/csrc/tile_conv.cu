@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "jt_blocks.cuh"
+#include "pw_bww.h"
 #include "tile_conv.h"
 
 namespace spc {
@@ -313,7 +314,13 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
     // JTP: jump-table kernel with packed f32x2 blocks -- accumulators and taps
     // live as 64-bit channel pairs for the whole pass (no in-line path)
     using JB2 = JtBlocks2<FWD, KK, TH, TW, R, S, STR>;
-    constexpr bool JTP = SPARSE && JT >= 100 && SPC_FFMA2 && JB2::available;
+    // JT == 200: "counted dense" -- every region pixel's FMAs execute (no
+    // per-pixel branch) while the zero test still runs for the exact counter;
+    // for geometries whose per-pixel blocks are too small for a branch to pay
+    // (3x3 stride-2 FWD: ~2.25 taps per source pixel).  Finite filters only
+    // (dispatch guards: 0*Inf would be NaN where the reference skips).
+    constexpr bool FORCE = JT == 200;
+    constexpr bool JTP = SPARSE && JT >= 100 && !FORCE && SPC_FFMA2 && JB2::available;
     constexpr int KA = JTP ? KK / 2 : KK;
     using AccT = std::conditional_t<JTP, unsigned long long, float>;
     using GV = std::conditional_t<JTP, FVecP<KK>, FVec<KK>>;
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
         for (int j = 0; j < KA; ++j) acc[t][j] = AccT(0);
 
     constexpr int NST = Gm::NST;
-    bool use_jt = JT >= 100;  // JT in 1..99: decided per block below, starting with branches
+    bool use_jt = JT >= 100 && !FORCE;  // JT in 1..99: decided per block below, starting with branches
 #pragma unroll
     for (int d = 0; d < NST - 1; ++d) {
         if (d < CiB) stage(d, d);
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
                 jt_words<0, NWORD, JB2>(acc, g, vv, m);
             } else {
             if (use_jt) {
-                if constexpr (SPARSE && JT > 0 && JB::available) jt_words<0, NWORD, JB>(acc, g, vv, m);
+                if constexpr (SPARSE && JT > 0 && !FORCE && JB::available) jt_words<0, NWORD, JB>(acc, g, vv, m);
             } else {
             const float* Pw = P + woff;
             float4 cur[NQ], nxt[NQ];
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
 #pragma unroll
                 for (int rx = 0; rx < RWW; ++rx) {
                     const int p = ry * RWW + rx;
-                    if (!SPARSE || ((m[p >> 5] >> (p & 31)) & 1u)) {
+                    if (!SPARSE || FORCE || ((m[p >> 5] >> (p & 31)) & 1u)) {
                         const float4 q4 = cur[rx >> 2];
                         const float d = (rx & 3) == 0 ? q4.x : (rx & 3) == 1 ? q4.y : (rx & 3) == 2 ? q4.z : q4.w;
                         int ntap = 0;  // folds to a constant per unrolled pixel
@@ -516,7 +523,9 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
     const int Ci = FWD ? sh.C : sh.K;
     const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
     const size_t src_bytes = (size_t)sh.N * Ci * Hs * Ws * sizeof(float);
-    const int group_fastest = src_bytes > ((size_t)48 << 20) ? 1 : 0;
+    // SPC_GROUP_FASTEST=0/1 forces the block order (A/B testing only)
+    static const int gf_env = std::getenv("SPC_GROUP_FASTEST") ? std::atoi(std::getenv("SPC_GROUP_FASTEST")) : -1;
+    const int group_fastest = gf_env >= 0 ? gf_env : (src_bytes > ((size_t)48 << 20) ? 1 : 0);
     kern<<<grid, Gm::NT, Gm::SMEM, st>>>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest, epi, gate);
     note_launch();
     return cudaGetLastError();
@@ -715,6 +724,30 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
     }
     if (sh.R == 3) {  // stride 2
         if (fwd) {
+            if (sparse && xsel == nullptr) {
+                // a stride-2 source pixel feeds ~2.25 taps: per-pixel branches cost more
+                // than the FMAs they skip, so finite filters run the counted-dense
+                // kernel (JT = 200); a filter with Inf/NaN keeps the per-pixel skip
+                int* finite = nullptr;
+                cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+                if (e != cudaSuccess) return e;
+                launch_finite_all(filt, (size_t)sh.K * sh.C * 9, finite, st);
+                if (kk4) {
+                    e = launch_cfg<true, 4, 4, 4, 2, 1, 3, 3, 2, 1, 200, true>(true, sh, src, filt, dst, exec_ctr, st,
+                                                                              finite, 1, epi, gate);
+                    if (e == cudaSuccess)
+                        e = launch_cfg<true, 4, 4, 4, 2, 1, 3, 3, 2, 1, 0, true>(true, sh, src, filt, dst, exec_ctr,
+                                                                                st, finite, 0, epi, gate);
+                } else {
+                    e = launch_cfg<true, 2, 4, 4, 2, 1, 3, 3, 2, 1, 200, true>(true, sh, src, filt, dst, exec_ctr, st,
+                                                                              finite, 1, epi, gate);
+                    if (e == cudaSuccess)
+                        e = launch_cfg<true, 2, 4, 4, 2, 1, 3, 3, 2, 1, 0, true>(true, sh, src, filt, dst, exec_ctr,
+                                                                                st, finite, 0, epi, gate);
+                }
+                cudaFreeAsync(finite, st);
+                return e;
+            }
             if (kk4) SPC_L(true, 4, 4, 4, 2, 1, 3, 2);
             SPC_L(true, 2, 4, 4, 2, 1, 3, 2);
         }

@@ -471,15 +471,17 @@ def test_baseline_layers_match_reference_cpu(sp, cfg, idx):
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 @pytest.mark.parametrize("comp", [0, 1])
 @pytest.mark.parametrize("stride", [1, 2])
-def test_pointwise_nonfinite_filter_keeps_skip_semantics(sp, comp, stride):
-    """The 1x1 kernel executes zero products (exact for finite filters); a filter
-    with Inf/NaN must still follow the reference's skip semantics (0 inputs are
-    skipped, so 0*Inf never happens): GPU == reference CPU incl. NaN/Inf positions."""
+@pytest.mark.parametrize("R", [1, 3])
+def test_pointwise_nonfinite_filter_keeps_skip_semantics(sp, comp, stride, R):
+    """The 1x1 kernels and the 3x3 stride-2 FWD kernel execute zero products
+    (exact for finite filters); a filter with Inf/NaN must still follow the
+    reference's skip semantics (0 inputs are skipped, so 0*Inf never happens):
+    GPU == reference CPU incl. NaN/Inf positions."""
     V = 16
-    sh = sp.ConvShape.make(3, 64, 128, 9, 10, 1, 1, stride, stride)
-    rng = np.random.default_rng(11 + comp + stride)
+    sh = sp.ConvShape.make(3, 64, 128, 9, 10, R, R, stride, stride)
+    rng = np.random.default_rng(11 + comp + stride + R)
     hp, wp = sh.out_h(), sh.out_w()
-    G = rng.standard_normal((sh.K, sh.C, 1, 1)).astype(np.float32)
+    G = rng.standard_normal((sh.K, sh.C, R, R)).astype(np.float32)
     if comp == 0:
         X = np.maximum(rng.standard_normal((sh.N, sh.C, sh.H, sh.W)), 0).astype(np.float32)
         X[:, 5] = 0.0       # channel 5 all zero: its Inf/NaN weights must be skipped
