@@ -12,11 +12,21 @@ def family(name):
     m = re.search(r"<([^>]*)>\(", name)
     args = [a.strip().replace("(bool)", "").replace("(int)", "") for a in m.group(1).split(",")] if m else []
     if args and n.endswith("tile_conv_kernel"):
-        n += ("<FWD>" if args[0] in ("1", "true") else "<BWI>") + ("[sparse]" if args[-1] in ("1", "true") else "[dense]")
+        # <FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, SPARSE, EPI>
+        sparse = args[11] if len(args) > 12 else args[-1]
+        jt = args[10] if len(args) > 10 else "0"
+        kind = "[jump-table]" if jt == "100" else "[counted-dense]" if jt == "200" else ""
+        n += ("<FWD>" if args[0] in ("1", "true") else "<BWI>") + ("[sparse]" if sparse in ("1", "true") else "[dense]")
+        n += kind
     elif args and n.endswith("bww_tile_kernel"):
         n += ("<check=input>" if args[0] in ("1", "true") else "<check=output_grad>")
         n += "[sparse]" if args[-1] in ("1", "true") else "[dense]"
     return n
+
+
+# setup-only kernels of tools/one_step.py (synthetic data, packing, the BWW
+# operand's ActCHWNn copy): not part of the timed bench step
+SETUP = ("at::", "nchwc_to_chwnn")
 
 
 def main(path, out_json=None):
@@ -31,6 +41,8 @@ def main(path, out_json=None):
         unit = r[iu]
         us = v / 1000.0 if unit in ("ns", "nsecond") else v * 1000.0 if unit in ("ms", "msecond") else v
         f = family(r[ik])
+        if any(f.startswith(x) or x in f for x in SETUP):
+            continue
         agg[f][0] += 1
         agg[f][1] += us
     tot = sum(v[1] for v in agg.values())
@@ -39,7 +51,9 @@ def main(path, out_json=None):
     for k, v in res.items():
         print(f"{v['share']*100:6.2f}%  {v['total_us']:12.1f} us  {v['launches']:5d}  {k}")
     if out_json:
-        json.dump({"source": path, "total_us": round(tot, 1), "kernels": res}, open(out_json, "w"), indent=1)
+        json.dump({"source": path, "note": "one bench step (tools/one_step.py) under ncu --metrics gpu__time_duration.sum "
+                   "--clock-control none; setup kernels excluded; per-launch times are cold-cache and serialised",
+                   "total_us": round(tot, 1), "kernels": res}, open(out_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
