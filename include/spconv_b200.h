@@ -154,6 +154,18 @@ spc_status spc_sparse_bwi_ex(const spc_tensor* grad_out, const spc_tensor* filt_
 /* The same epilogue as a standalone pass over n elements of `data` (in place). */
 spc_status spc_epilogue_apply(const spc_epilogue* epi, float* data, size_t n, void* stream);
 
+/* ---- arithmetic of the passes (no reference counterpart) ----
+ * SPC_MATH_FP32 (default): FP32 CUDA-core FFMA, zero skipping, the reference's
+ * per-product rounding.  SPC_MATH_TF32X3: tcgen05 tensor cores with 3xTF32
+ * split products (hi*hi + hi*lo + lo*hi, fp32 accumulate), its own stated
+ * tolerance; used for the geometries it covers (V = 16,
+ * stride 1, 3x3 pad 1 / 1x1 pad 0), the FP32 kernels elsewhere and for
+ * inputs holding Inf/NaN.  Per host thread; returns the previous mode, or -1
+ * for an unknown mode (unchanged). */
+typedef enum { SPC_MATH_FP32 = 0, SPC_MATH_TF32X3 = 1 } spc_math;
+int spc_set_math(int math);
+int spc_get_math(void);
+
 /* ---- host-buffer drop-ins: copy in, run, copy out, synchronize ---- */
 spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters);

@@ -49,6 +49,8 @@ _SIGS = {
     "spc_backend_name": (C.c_char_p, []),
     "spc_native_backend_available": (C.c_int, [C.c_int]),
     "spc_launch_count": (C.c_uint64, []),
+    "spc_set_math": (C.c_int, [C.c_int]),
+    "spc_get_math": (C.c_int, []),
     "spc_shape_make": (C.c_int, [C.c_int] * 9 + [C.POINTER(spc_shape)]),
     "spc_shape_make_padded": (C.c_int, [C.c_int] * 11 + [C.POINTER(spc_shape)]),
     "spc_shape_validate": (C.c_int, [C.POINTER(spc_shape)]),

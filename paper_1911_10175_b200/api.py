@@ -25,6 +25,7 @@ Contract violations raise :class:`SpconvError` (the analogue of
 from __future__ import annotations
 
 import ctypes as C
+import contextlib
 import dataclasses
 import enum
 from typing import Any
@@ -395,6 +396,36 @@ def backend_names() -> list[str]:
 
 def launch_count() -> int:
     return int(_lib.load().spc_launch_count())
+
+
+class Math(enum.IntEnum):
+    """Arithmetic of FWD/BWI (``spc_set_math``): ``fp32`` = FP32 FFMA with
+    zero skipping (default, the reference's per-product rounding); ``tf32x3``
+    = tcgen05 tensor cores with 3xTF32 split products (its own tolerance,
+    DESIGN.md 4.7).  Per host thread."""
+    fp32 = 0
+    tf32x3 = 1
+
+
+def set_math(m: Math) -> Math:
+    prev = _lib.load().spc_set_math(int(m))
+    if prev < 0:
+        raise SpconvError(_lib.SPC_ERR_ARG, f"unknown math mode {m!r}")
+    return Math(prev)
+
+
+def get_math() -> Math:
+    return Math(_lib.load().spc_get_math())
+
+
+@contextlib.contextmanager
+def math_mode(m: Math):
+    """``with math_mode(Math.tf32x3): ...`` -- restores the previous mode."""
+    prev = set_math(m)
+    try:
+        yield
+    finally:
+        set_math(prev)
 
 
 @dataclasses.dataclass

@@ -583,6 +583,14 @@ spc_status spc_sparse_bwi_ex(const spc_tensor* grad_out, const spc_tensor* filt_
     return run_fwd_bwi(false, grad_out, filt_t, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream, epi);
 }
 
+int spc_set_math(int math) {
+    if (math != SPC_MATH_FP32 && math != SPC_MATH_TF32X3) return -1;
+    const int prev = math_mode();
+    set_math_mode(math);
+    return prev;
+}
+int spc_get_math(void) { return math_mode(); }
+
 spc_status spc_epilogue_apply(const spc_epilogue* epi, float* data, size_t n, void* stream) {
     spc_status s = check_epi(epi);
     if (s) return s;

@@ -6,10 +6,17 @@
 #include "pw_bww.h"
 #include "pw_conv.h"
 #include "pw_gemm.h"
+#include "tc_conv.h"
 #include "tile_bww.h"
 #include "tile_conv.h"
 
 namespace spc {
+
+// Arithmetic of the FWD/BWI passes (spc_set_math): FP32 FFMA (default) or the
+// 3xTF32 tensor-core variant.  Per host thread, like spc_last_error.
+static thread_local int g_math = SPC_MATH_FP32;
+int math_mode() { return g_math; }
+void set_math_mode(int m) { g_math = m; }
 
 __global__ void epilogue_kernel(Epi epi, float* __restrict__ out, size_t n) {
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
@@ -42,6 +49,8 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
     // SPC_PW_OFF=1 routes 1x1 convs to the tile kernel (A/B testing only)
     static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
+    if (g_math == SPC_MATH_TF32X3 && gate.in_ready == nullptr && tc_conv_supported(fwd, sh, V))
+        return launch_tc_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);
     if (!force_generic && !pw_off && use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) {
         int* finite = nullptr;
         cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);

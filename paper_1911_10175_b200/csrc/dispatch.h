@@ -7,6 +7,9 @@
 
 namespace spc {
 
+int math_mode();
+void set_math_mode(int m);
+
 // FWD (fwd=true) or BWI: picks the tuned V=16 tile kernel when the geometry
 // has one, else the shape-general kernel.
 cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const float* src, const float* filt,

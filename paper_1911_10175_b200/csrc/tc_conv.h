@@ -1,0 +1,9 @@
+// tc_conv.h -- 3xTF32 tcgen05 FWD/BWI (internal).
+#pragma once
+#include "common.cuh"
+
+namespace spc {
+bool tc_conv_supported(bool fwd, const DevShape& sh, int V);
+cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
+                           float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi);
+}  // namespace spc

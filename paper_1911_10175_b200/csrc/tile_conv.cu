@@ -772,4 +772,32 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
 #undef SPC_L
 }
 
+// FFMA tile kernel gated on a device word (*sel == want), used behind the
+// tensor-core variant for sources / filters with Inf or NaN (tc_conv.cu).
+cudaError_t launch_tile_conv_when(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
+                                  float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi,
+                                  const int* sel, int want) {
+    const bool kk4 = (fwd ? sh.K : sh.C) % 128 == 0;
+    if (sh.R == 3) {
+        if (kk4)
+            return fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                              sel, want, epi, Gate{})
+                       : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr,
+                                                                               st, sel, want, epi, Gate{});
+        return fwd ? launch_cfg<true, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, sel,
+                                                                          want, epi, Gate{})
+                   : launch_cfg<false, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                           sel, want, epi, Gate{});
+    }
+    if (kk4)
+        return fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 1, 1, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, sel,
+                                                                          want, epi, Gate{})
+                   : launch_cfg<false, 4, 4, 8, 2, 1, 1, 1, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                           sel, want, epi, Gate{});
+    return fwd ? launch_cfg<true, 2, 4, 8, 2, 1, 1, 1, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, sel,
+                                                                      want, epi, Gate{})
+               : launch_cfg<false, 2, 4, 8, 2, 1, 1, 1, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, sel,
+                                                                       want, epi, Gate{});
+}
+
 }  // namespace spc

@@ -1,0 +1,128 @@
+"""GPU parity of the 3xTF32 tensor-core variant (spc_set_math(SPC_MATH_TF32X3),
+SURVEY.md 8(f)4) against the 64-bit oracle.
+
+Stated tolerance of the variant: max|got - ref| / max|ref|
+<= TC_TOL = 1e-5 -- the north-star fp32 gate itself; 3xTF32 products carry
+~2^-21 relative error, measured ~1e-7 here.  Counters (executed_vector_fmas,
+checked_vectors) stay integer-exact; Inf/NaN inputs take the exact FFMA path.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+TC_TOL = 1e-5
+V = 16
+
+
+def _gauss_relu(rng, shape, s):
+    x = rng.standard_normal(shape).astype(np.float32)
+    x[rng.random(shape) < s] = 0.0
+    return x
+
+
+def _run(sp, sh, comp, a, b, mode=0, math=None, epi=None):
+    math = sp.Math.tf32x3 if math is None else math
+    if comp == 0:
+        ba, bb = sp.pack_act_nchwc(a, V), sp.pack_filter(b, V)
+    else:
+        ba, bb = sp.pack_act_nchwc(a, V), sp.pack_filter(b, V, True)
+    ba, bb = ba.to("cuda"), bb.to("cuda")
+    pl = sp.plan(sh, sp.Component(comp), V)
+    with sp.math_mode(math):
+        res = sp.run_parallel(ba, bb, sh, pl, sp.RunMode(mode))
+    return pl, res, sp.unpack(res.out).cpu().numpy()
+
+
+SHAPES = [
+    (2, 64, 64, 56, 56, 3, 3),
+    (2, 128, 256, 28, 28, 3, 3),
+    (1, 256, 128, 14, 14, 3, 3),
+    (3, 64, 128, 13, 9, 3, 3),
+    (2, 512, 512, 7, 7, 3, 3),
+    (2, 128, 64, 20, 36, 1, 1),
+    (1, 256, 512, 14, 14, 1, 1),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("comp", [0, 1])
+def test_tc_matches_oracle(sp, shape, comp):
+    rng = np.random.default_rng(hash((shape, comp)) & 0xFFFF)
+    N, C, K, H, W, R, S = shape
+    sh = sp.ConvShape.make(N, C, K, H, W, R, S, 1, 1)
+    t = sh.astuple()
+    if comp == 0:
+        a = _gauss_relu(rng, (N, C, H, W), 0.6)
+    else:
+        a = _gauss_relu(rng, (N, K, sh.out_h(), sh.out_w()), 0.5)
+    g = (rng.standard_normal((K, C, S, R)) * np.sqrt(2.0 / (C * R * S))).astype(np.float32)
+    ref = O.dense(comp, t, a, g)
+    pl, res, got = _run(sp, sh, comp, a, g)
+    err = O.max_abs_rel(got, ref)
+    assert err <= TC_TOL, (shape, comp, err)
+    want = O.expected_counts(t, O.plan(t, comp, V, 30, 0), a)
+    assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+    assert res.counters.checked_vectors == want["checked_vectors"]
+    # dense mode: same arithmetic, analytic dense total
+    _, dres, dgot = _run(sp, sh, comp, a, g, mode=1)
+    assert np.array_equal(dgot, got)
+    assert dres.counters.executed_vector_fmas == want["dense_total"]
+
+
+def test_tc_is_deterministic_and_close_to_fp32_path(sp):
+    rng = np.random.default_rng(3)
+    sh = sp.ConvShape.make(2, 128, 128, 28, 28, 3, 3, 1, 1)
+    a = _gauss_relu(rng, (2, 128, 28, 28), 0.5)
+    g = (rng.standard_normal((128, 128, 3, 3)) * 0.04).astype(np.float32)
+    _, _, g1 = _run(sp, sh, 0, a, g)
+    _, _, g2 = _run(sp, sh, 0, a, g)
+    _, _, f32 = _run(sp, sh, 0, a, g, math=sp.Math.fp32)
+    assert np.array_equal(g1, g2)
+    assert O.max_abs_rel(g1, f32) <= TC_TOL
+
+
+@pytest.mark.parametrize("where", ["src_nan", "src_inf", "filt_inf"])
+def test_tc_nonfinite_inputs_take_exact_path(sp, where):
+    rng = np.random.default_rng(11)
+    sh = sp.ConvShape.make(1, 64, 128, 12, 12, 3, 3, 1, 1)
+    a = _gauss_relu(rng, (1, 64, 12, 12), 0.5)
+    g = (rng.standard_normal((128, 64, 3, 3)) * 0.05).astype(np.float32)
+    if where == "src_nan":
+        a[0, 3, 4, 5] = np.nan
+    elif where == "src_inf":
+        a[0, 7, 0, 0] = np.inf
+    else:
+        a[0, 9, :, :] = 0.0  # an all-zero channel: the reference skips it, so Inf taps there stay harmless
+        g[5, 9, 1, 1] = np.inf
+    _, r32, f32 = _run(sp, sh, 0, a, g, math=sp.Math.fp32)
+    _, rtc, tc = _run(sp, sh, 0, a, g)
+    assert np.array_equal(np.isnan(tc), np.isnan(f32))
+    assert np.array_equal(np.isinf(tc), np.isinf(f32))
+    assert np.array_equal(tc, f32) or O.max_abs_rel(np.nan_to_num(tc), np.nan_to_num(f32)) <= TC_TOL
+    assert rtc.counters.executed_vector_fmas == r32.counters.executed_vector_fmas
+
+
+def test_tc_fused_epilogue(sp):
+    import torch
+    rng = np.random.default_rng(5)
+    sh = sp.ConvShape.make(2, 64, 128, 14, 14, 3, 3, 1, 1)
+    a = _gauss_relu(rng, (2, 64, 14, 14), 0.5)
+    g = (rng.standard_normal((128, 64, 3, 3)) * 0.06).astype(np.float32)
+    add = _gauss_relu(rng, (2, 128, 14, 14), 0.0)
+    mask = _gauss_relu(rng, (2, 128, 14, 14), 0.5)
+    ba, bb = sp.pack_act_nchwc(a, V).to("cuda"), sp.pack_filter(g, V).to("cuda")
+    badd, bmask = sp.pack_act_nchwc(add, V).to("cuda"), sp.pack_act_nchwc(mask, V).to("cuda")
+    pl = sp.plan(sh, sp.Component.fwd, V)
+    epi = sp.Epilogue(alpha=0.25, add=badd.data, mask=bmask.data, relu=True)
+    outs = []
+    for m in (sp.Math.fp32, sp.Math.tf32x3):
+        with sp.math_mode(m):
+            p = sp.PreparedPass(ba, bb, sh, pl, epilogue=epi)
+            p.launch(torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            outs.append(p.out.cpu().numpy().copy())
+    f32, tc = outs
+    assert np.array_equal(f32 == 0, tc == 0) or np.mean((f32 == 0) != (tc == 0)) < 1e-4
+    assert O.max_abs_rel(tc, f32) <= TC_TOL

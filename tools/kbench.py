@@ -28,11 +28,18 @@ def main():
     ap.add_argument("--sparsity", type=float, nargs="+", default=[0.5])
     ap.add_argument("--layers", type=int, default=99)
     ap.add_argument("--bww-check", default="input")
+    ap.add_argument("--math", default="fp32", choices=["fp32", "tf32x3"])
+    ap.add_argument("--comps", nargs="+", default=["fwd", "bwi", "bww"])
+    ap.add_argument("--config-layers", type=int, nargs="*", default=None, help="layer indices to run")
     args = ap.parse_args()
+    sp.set_math(sp.Math[args.math])
     V = 16
     g = torch.Generator(device="cuda").manual_seed(0)
     stream = torch.cuda.current_stream()
-    for layer in wl.CONFIGS[args.config]()[: args.layers]:
+    layers = wl.CONFIGS[args.config]()[: args.layers]
+    if args.config_layers:
+        layers = [layers[i] for i in args.config_layers]
+    for layer in layers:
         sh = layer.shape
         flops = sh.dense_flops()
         G = wl.device_weights(sh.K, sh.C, sh.S, sh.R, g)
@@ -46,6 +53,8 @@ def main():
             }
             row = []
             for name, (a, b, chk) in ops.items():
+                if name not in args.comps:
+                    continue
                 comp = sp.Component[name]
                 pl = sp.plan(sh, comp, V, 30, chk)
                 t_s = time_pass(sp.PreparedPass(a, b, sh, pl, sp.RunMode.sparse), stream)

@@ -18,7 +18,9 @@ ap.add_argument("--sparsity", type=float, default=0.5)
 ap.add_argument("--mode", default="sparse")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--math", default="fp32", choices=["fp32", "tf32x3"])
 a = ap.parse_args()
+sp.set_math(sp.Math[a.math])
 V = 16
 sh = wl.CONFIGS[a.config]()[a.layer].shape
 if a.batch:
