@@ -83,6 +83,8 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
                        const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
     static const bool force_generic = std::getenv("SPC_FORCE_GENERIC") && std::atoi(std::getenv("SPC_FORCE_GENERIC"));
     static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
+    if (g_math == SPC_MATH_TF32X3 && tc_bww_supported(sh, V))
+        return launch_tc_bww(check_input, sparse, sh, chk, oth, dst, exec_ctr, st);
     if (!force_generic && !pw_off && pw_bww_supported(check_input, sh, V)) {
         int* finite = nullptr;
         cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);

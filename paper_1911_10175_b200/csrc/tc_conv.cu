@@ -45,113 +45,20 @@
 
 #include "common.cuh"
 #include "pw_bww.h"
+#include "tc_common.cuh"
 #include "tc_conv.h"
+#include "tile_bww.h"
 #include "tile_conv.h"
 
 namespace spc {
 namespace {
+using namespace tc;
 
 constexpr int TC_BM = 128;
 constexpr int TC_ST = 4;          // pipeline stages
 constexpr int TC_THREADS = 320;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// ---------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-// Same, with a back-off: for the epilogue warps, which wait a whole segment
-// and would otherwise take issue slots from the producer / MMA threads.
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-    uint32_t ok = 0;
-    for (;;) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-        if (ok) break;
-        __nanosleep(256);
-    }
-}
-__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
-                                            int c2, int c3, int c4) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
-                                            int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-        : "memory");
-}
-// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: rows of 64 bytes,
-// 8-row groups 512 bytes apart (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
-    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(512 >> 4) << 32;     // SBO
-    d |= (uint64_t)1 << 46;              // version
-    d |= (uint64_t)4 << 61;              // SWIZZLE_64B
-    return d;
-}
-// Instruction descriptor: kind::tf32, D = f32, A/B K-major, M = 128, N = BN.
-template <int BN>
-__device__ __forceinline__ uint32_t tf32_idesc() {
-    return (1u << 4)                        // D format f32
-           | (2u << 7) | (2u << 10)         // A, B = tf32
-           | ((uint32_t)(BN >> 3) << 17)    // N
-           | ((uint32_t)(TC_BM >> 4) << 24);  // M
-}
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-}
+// TMEM allocations are powers of two >= 32 columns
+constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 
 // Geometry of one launch, by value.
 struct TcGeo {
@@ -216,7 +123,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(2 * BN)
+                     "n"(tmem_cols(2 * BN))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -333,7 +240,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN)) : "memory");
     }
 }
 
@@ -348,12 +255,14 @@ __global__ void tc_split_src_kernel(const float* __restrict__ src, float* __rest
     int bad = 0;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n4; e += (size_t)gridDim.x * blockDim.x) {
         const float4 x = __ldg(reinterpret_cast<const float4*>(src) + e);
-        float4 l;
-        l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-        l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-        l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-        l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-        reinterpret_cast<float4*>(lo)[e] = l;
+        if (lo) {
+            float4 l;
+            l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+            l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+            l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+            l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+            reinterpret_cast<float4*>(lo)[e] = l;
+        }
         bad |= !isfinite(x.x) | !isfinite(x.y) | !isfinite(x.z) | !isfinite(x.w);
         const unsigned nz = (x.x != 0.0f) + (x.y != 0.0f) + (x.z != 0.0f) + (x.w != 0.0f);
         if (nz && cnt) {
@@ -410,28 +319,6 @@ __global__ void tc_zero_kernel(int* flag, unsigned long long* cnt) {
 }
 
 // ---------------------------------------------------------------- host
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-// ActNCHWc [N][CB][H][W][16] as a 5-D map, box = 16 ch x bw x bh x 1 x 1.
-bool make_act_map(CUtensorMap* m, const float* p, int N, int CB, int H, int W, int bw, int bh) {
-    cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)CB, (cuuint64_t)N};
-    cuuint64_t strides[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)CB * H * W * 64};
-    cuuint32_t box[5] = {16, (cuuint32_t)bw, (cuuint32_t)bh, 1, 1};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(p), dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 // K-major filter copy [taps*RB][Co][16], box = 16 x bn x 1.
 bool make_filter_map(CUtensorMap* m, const float* p, int rows, int Co, int bn) {
     cuuint64_t dims[3] = {16, (cuuint64_t)Co, (cuuint64_t)rows};
@@ -475,6 +362,282 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     return cudaGetLastError();
 }
 
+// ================================================================ BWW
+// dG[k, c, v, u] = sum_{i, y', x'} dY[i, k, y', x'] * D[i, c, y'+v-padH, x'+u-padW]
+// (P/src/kernel_impl.hpp:209-336, P/src/kernels.cpp:238-302), as one GEMM per
+// tap: M = 128 output-gradient channels k, N = BN input channels c, reduction
+// over (image, output pixel).  The prep kernels rewrite both operands (hi =
+// raw, lo = split remainder) pixel-major, [N/16][H][W][C][16 images] -- the
+// reference's ActCHWNn with the channel loop moved inside the pixel, so one
+// pixel of one 16-image block is C x 64 contiguous bytes: a stage = one
+// pixel, the A tile {16 images, 128 k} / B tile {16 images, BN c} are single
+// contiguous TMA boxes that land in shared memory as K-major SWIZZLE_64B
+// operands exactly like the FWD tiles.  Pixels outside the image are TMA
+// zero-fill (the padding); ragged image lanes are zeros.
+// A CTA owns (tap, k tile, c tile, reduction split); partial tiles go to
+// scratch and a fixed-order reduction writes FilterKCRSblk (deterministic).
+struct TcBwwGeo {
+    int Hp, Wp;      // output (dY) extent
+    int R, S, padW, padH;
+    int K, C;
+    int ktiles, ctiles, splits;
+    int cw, tpc, tgroups;  // channels per tap in a c tile, taps stacked along N (BN = tpc * cw), tap groups
+    long stages;     // ceil(N / 16) * Hp * Wp
+    int seg;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_bww_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                  const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                  TcBwwGeo g, float* __restrict__ partial, const int* __restrict__ nonfinite,
+                  const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr) {
+    if (__ldg(nonfinite) != 0) return;
+    constexpr uint32_t A_BYTES = TC_BM * 64;  // 8 k-blocks x 16 px x 64 B
+    constexpr uint32_t B_BYTES = BN * 64;     // BN/16 c-blocks x 16 px x 64 B
+    constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
+    constexpr int HALF = BN / 2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_ST * STAGE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_ST + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // blockIdx.x = ((tap * ktiles + kt) * ctiles + ct), blockIdx.y = split
+    int b = blockIdx.x;
+    const int ct = b % g.ctiles;
+    b /= g.ctiles;
+    const int kt = b % g.ktiles;
+    const int tg = b / g.ktiles;  // taps tg*tpc .. +tpc-1 stacked along N
+    const int split = blockIdx.y;
+    const long t0 = g.stages * split / g.splits, t1 = g.stages * (split + 1) / g.splits;
+    const int niter = (int)(t1 - t0);
+    const int D = g.seg;
+    const int nseg = (niter + D - 1) / D;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (TC_ST + s); };
+    auto tfull_bar = [&](int bb) { return bar0 + 8u * (2 * TC_ST + bb); };
+    auto tempty_bar = [&](int bb) { return bar0 + 8u * (2 * TC_ST + 2 + bb); };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int bb = 0; bb < 2; ++bb) {
+            mbar_init(tfull_bar(bb), 1);
+            mbar_init(tempty_bar(bb), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (blockIdx.x == 0 && blockIdx.y == 0 && cnt_tmp && exec_ctr) atomicAdd(exec_ctr, *cnt_tmp);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(tmem_cols(2 * BN))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0 && niter > 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+            long t = t0;
+            int ib = (int)(t / ((long)g.Hp * g.Wp));
+            int rem = (int)(t - (long)ib * g.Hp * g.Wp);
+            int yp = rem / g.Wp, xp = rem - yp * g.Wp;
+            for (int it = 0; it < niter; ++it) {
+                const int s = it % TC_ST;
+                if (it >= TC_ST) mbar_wait(empty_bar(s), ((it / TC_ST) - 1) & 1);
+                const uint32_t st = sbase + s * STAGE;
+                mbar_expect_tx(full_bar(s), STAGE);
+                tma_load_5d(st, &map_ahi, full_bar(s), 0, kt * TC_BM, xp, yp, ib);
+                tma_load_5d(st + A_BYTES, &map_alo, full_bar(s), 0, kt * TC_BM, xp, yp, ib);
+                for (int j = 0; j < g.tpc; ++j) {
+                    const int tap = tg * g.tpc + j;
+                    const int v = tap / g.R, u = tap - v * g.R;
+                    // a missing tap of the last group loads an all-out-of-bounds box (zeros)
+                    const int sx = tap < g.R * g.S ? xp + u - g.padW : -(1 << 20), sy = yp + v - g.padH;
+                    const uint32_t boff = (uint32_t)(j * g.cw * 64);
+                    tma_load_5d(st + 2 * A_BYTES + boff, &map_bhi, full_bar(s), 0, ct * g.cw, sx, sy, ib);
+                    tma_load_5d(st + 2 * A_BYTES + B_BYTES + boff, &map_blo, full_bar(s), 0, ct * g.cw, sx, sy, ib);
+                }
+                if (++xp == g.Wp) {
+                    xp = 0;
+                    if (++yp == g.Hp) {
+                        yp = 0;
+                        ++ib;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tf32_idesc<BN>();
+            for (int it = 0; it < niter; ++it) {
+                const int seg = it / D, buf = seg & 1;
+                const bool first = it - seg * D == 0;
+                if (first && seg >= 2) mbar_wait(tempty_bar(buf), ((seg >> 1) - 1) & 1);
+                const int s = it % TC_ST;
+                mbar_wait(full_bar(s), (it / TC_ST) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t st = sbase + s * STAGE;
+                const uint32_t tm = tmem + buf * BN;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {  // images 0-7, 8-15 (32 bytes each)
+                    const uint64_t ahi = sw64_desc(st + 32 * k);
+                    const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
+                    const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
+                    const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + 32 * k);
+                    umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
+                    umma_tf32(tm, ahi, blo, idesc, 1u);
+                    umma_tf32(tm, ahi, bhi, idesc, 1u);
+                }
+                umma_commit(empty_bar(s));
+                if (it - seg * D == D - 1 || it == niter - 1) umma_commit(tfull_bar(buf));
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int krow = kt * TC_BM + q * 32 + lane;
+        float acc[HALF];
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        for (int seg = 0; seg < nseg; ++seg) {
+            const int buf = seg & 1;
+            mbar_wait_sleep(tfull_bar(buf), (seg >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < HALF / 16; ++j) {
+                float vv[16];
+                tmem_ld16(tmem + lane_off + buf * BN + h * HALF + 16 * j, vv);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) acc[16 * j + e] += vv[e];
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar(buf));
+        }
+        // partial[split][tap][k][c] (k < K, c < C, existing taps only); column
+        // n of the tile = (tap tg*tpc + n / cw, channel ct*cw + n % cw)
+        if (krow < g.K) {
+#pragma unroll
+            for (int j = 0; j < HALF; j += 4) {
+                const int n = h * HALF + j;
+                const int tj = n / g.cw, c = ct * g.cw + (n - tj * g.cw);
+                const int tap = tg * g.tpc + tj;
+                if (tap < g.R * g.S && c < g.C) {
+                    float* o = partial + (((size_t)split * g.R * g.S + tap) * g.K + krow) * g.C + c;
+                    *reinterpret_cast<float4*>(o) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN)) : "memory");
+    }
+}
+
+// Fixed-order sum over splits -> FilterKCRSblk (K, C) (P/include/spconv/tensor.hpp:112-119).
+__global__ void tc_bww_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dst, int splits, int K,
+                                     int C, int R, int S, const int* __restrict__ nonfinite) {
+    if (__ldg(nonfinite) != 0) return;
+    const size_t n = (size_t)R * S * K * C;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int p = 0; p < splits; ++p) s += partial[(size_t)p * n + e];
+        const int c = (int)(e % C);
+        const int k = (int)((e / C) % K);
+        const int tap = (int)(e / ((size_t)C * K));
+        const int v = tap / R, u = tap - v * R;
+        dst[filter_index(C, S, R, 16, k, c, u, v)] = s;
+    }
+}
+
+// ActNCHWc [N][C/16][H][W][16] (FROM_CHWNN = false) or ActCHWNn
+// [N/16][C][H][W][16 images] (true) -> pixel-major [N/16][H][W][C][16 images]
+// hi (raw) + lo copies, ragged image lanes zero (the lane rule of
+// pack_act_chwnn, P/src/tensor.cpp:94-108).  A CTA moves one (16-image block,
+// 16-channel block, 16-pixel run) through a shared 16 x 16 x 16 tile: 1 KB
+// contiguous reads (16 px x 16 ch of one image, or 16 px x 16 images of one
+// channel) and 1 KB contiguous writes (16 ch x 16 images of one pixel).
+// Flags non-finite values.
+template <bool FROM_CHWNN>
+__global__ void tc_to_hwcn_split_kernel(const float* __restrict__ in, float* __restrict__ hi,
+                                        float* __restrict__ lo, int N, int C, int HW,
+                                        int* __restrict__ nonfinite) {
+    __shared__ float t[16 * 16 * 17];
+    const int pblocks = (HW + 15) / 16;
+    const int pb = blockIdx.x % pblocks;
+    const int cb = (blockIdx.x / pblocks) % (C / 16);
+    const int ib = blockIdx.x / (pblocks * (C / 16));
+    const int tid = threadIdx.x;
+    const int p0 = pb * 16;
+    const int px = tid >> 4, l = tid & 15;
+    int bad = 0;
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+        float x = 0.0f;
+        if (p0 + px < HW) {
+            if (FROM_CHWNN) {  // j = channel, l = image lane
+                x = __ldg(in + (((size_t)ib * C + cb * 16 + j) * HW + p0 + px) * 16 + l);
+                t[(px * 16 + j) * 17 + l] = x;
+            } else {           // j = image lane, l = channel
+                const int img = ib * 16 + j;
+                if (img < N) x = __ldg(in + (((size_t)img * (C / 16) + cb) * HW + p0 + px) * 16 + l);
+                t[(px * 16 + l) * 17 + j] = x;
+            }
+        } else {
+            t[(px * 16 + (FROM_CHWNN ? j : l)) * 17 + (FROM_CHWNN ? l : j)] = 0.0f;
+        }
+        bad |= !isfinite(x);
+    }
+    __syncthreads();
+    // write pixel p0 + p: channels cb*16 .. +15 x 16 images (1 KB contiguous)
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+        const int p = r, c = tid >> 4, i = tid & 15;
+        if (p0 + p >= HW) break;
+        const float x = t[(p * 16 + c) * 17 + i];
+        const size_t o = (((size_t)ib * HW + p0 + p) * C + cb * 16 + c) * 16 + i;
+        hi[o] = x;
+        lo[o] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(nonfinite, 1);
+}
+
+template <int BN>
+cudaError_t launch_bww_bn(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& bhi,
+                          const CUtensorMap& blo, const TcBwwGeo& g, float* partial, const int* nonfinite,
+                          const unsigned long long* cnt, unsigned long long* exec_ctr, cudaStream_t st) {
+    constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * BN * 64;
+    const size_t smem = TC_ST * STAGE + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tc_bww_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dim3 grid((unsigned)(g.tgroups * g.ktiles * g.ctiles), (unsigned)g.splits);
+    tc_bww_kernel<BN><<<grid, TC_THREADS, smem, st>>>(ahi, alo, bhi, blo, g, partial, nonfinite, cnt, exec_ctr);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool tc_conv_supported(bool fwd, const DevShape& sh, int V) {
@@ -485,7 +648,7 @@ bool tc_conv_supported(bool fwd, const DevShape& sh, int V) {
     if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
     const int Co = fwd ? sh.K : sh.C;
     if (Co % 64) return false;
-    return encode_fn() != nullptr;
+    return tc::encode_fn() != nullptr;
 }
 
 cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const float* src, const float* filt,
@@ -534,8 +697,8 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
 
     CUtensorMap mhi, mlo, mbhi, mblo;
     const int bn = Co % 256 == 0 ? 256 : (Co % 128 == 0 ? 128 : 64);
-    if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh) ||
-        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh) ||
+    if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, 1) ||
+        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, 1) ||
         !make_filter_map(&mbhi, bhi, taps * (Cr / 16), Co, bn) ||
         !make_filter_map(&mblo, blo, taps * (Cr / 16), Co, bn)) {
         cudaFreeAsync(scratch, st);
@@ -550,6 +713,112 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         e = launch_bn<64>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
     // non-finite source or filter: the FFMA tile kernel with the reference's exact skip semantics
     if (e == cudaSuccess) e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
+    cudaFreeAsync(scratch, st);
+    return e;
+}
+
+bool tc_bww_supported(const DevShape& sh, int V) {
+    if (V != 16) return false;
+    if (sh.O != 1 || sh.P != 1) return false;
+    if (!((sh.R == 3 && sh.S == 3) || (sh.R == 1 && sh.S == 1))) return false;
+    if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
+    if (sh.C % 16 || sh.K % 16) return false;
+    if ((sh.K % 64) || (sh.C % 64)) return false;  // the exact fallback (tile BWW) needs 64-channel multiples
+    return tc::encode_fn() != nullptr;
+}
+
+// check_input: chk = D (ActCHWNn), oth = dY (ActNCHWc); else chk = dY (ActCHWNn), oth = D (ActNCHWc).
+cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, const float* chk, const float* oth,
+                          float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+    const int HW = sh.H * sh.W, HWp = sh.Hp * sh.Wp;
+    const int NB = (sh.N + 15) / 16;
+    const size_t nD = (size_t)NB * 16 * sh.C * HW, nY = (size_t)NB * 16 * sh.K * HWp;  // CHWNn sizes
+    const int taps = sh.R * sh.S;
+    // N tile = tpc taps x cw channels: stacking taps keeps the MMA N (and the
+    // work per pipeline stage) large for 64/128-channel layers
+    const int cw = sh.C >= 256 ? 256 : sh.C;
+    const int tpc = taps == 1 ? 1 : (cw == 64 ? 3 : (cw == 128 ? 2 : 1));
+    const int BN = cw * tpc;
+    TcBwwGeo g;
+    g.cw = cw;
+    g.tpc = tpc;
+    g.tgroups = (taps + tpc - 1) / tpc;
+    g.Hp = sh.Hp;
+    g.Wp = sh.Wp;
+    g.R = sh.R;
+    g.S = sh.S;
+    g.padW = sh.padW;
+    g.padH = sh.padH;
+    g.K = sh.K;
+    g.C = sh.C;
+    g.ktiles = (sh.K + TC_BM - 1) / TC_BM;
+    g.ctiles = (sh.C + cw - 1) / cw;
+    g.stages = (long)NB * sh.Hp * sh.Wp;
+    const long tiles = (long)g.tgroups * g.ktiles * g.ctiles;
+    long splits = (148 + tiles - 1) / tiles;  // about one wave of CTAs
+    const long min_stages = 64;               // keep each split's pipeline long
+    if (splits > g.stages / min_stages) splits = g.stages / min_stages > 0 ? g.stages / min_stages : 1;
+    g.splits = (int)splits;
+    static const int seg_env = std::getenv("SPC_TC_SEG") ? std::atoi(std::getenv("SPC_TC_SEG")) : 0;
+    g.seg = seg_env > 0 ? seg_env : 8;
+    // scratch: [flag][counter] | D hi, D lo, dY hi, dY lo (pixel-major) | partials
+    const size_t nP = (size_t)g.splits * taps * sh.K * sh.C;
+    const size_t bytes = 256 + (2 * nD + 2 * nY) * 4 + nP * 4;
+    uint8_t* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&scratch, bytes, st);
+    if (e != cudaSuccess) return e;
+    int* nonfinite = reinterpret_cast<int*>(scratch);
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(scratch + 128);
+    float* d_hi = reinterpret_cast<float*>(scratch + 256);
+    float* d_lo = d_hi + nD;
+    float* y_hi = d_lo + nD;
+    float* y_lo = y_hi + nY;
+    float* part = y_lo + nY;
+    tc_zero_kernel<<<1, 1, 0, st>>>(nonfinite, cnt);
+    unsigned long long* cp = (sparse && exec_ctr) ? cnt : nullptr;
+    // exact executed_vector_fmas from the checked (ActCHWNn) operand -- its
+    // ragged lanes are zeros; then both operands -> pixel-major hi + lo
+    const unsigned tb_d = (unsigned)(NB * (sh.C / 16) * ((HW + 15) / 16));
+    const unsigned tb_y = (unsigned)(NB * (sh.K / 16) * ((HWp + 15) / 16));
+    if (check_input) {
+        if (cp)
+            tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(chk, nullptr, nD / 4, sh.H, sh.W, sh.Hp, sh.Wp, sh.R, sh.S,
+                                                         sh.padW, sh.padH, 0, (unsigned)(sh.K / 16), cp, nonfinite);
+        tc_to_hwcn_split_kernel<true><<<tb_d, 256, 0, st>>>(chk, d_hi, d_lo, sh.N, sh.C, HW, nonfinite);
+        tc_to_hwcn_split_kernel<false><<<tb_y, 256, 0, st>>>(oth, y_hi, y_lo, sh.N, sh.K, HWp, nonfinite);
+    } else {
+        if (cp)
+            tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(chk, nullptr, nY / 4, sh.Hp, sh.Wp, sh.H, sh.W, sh.R, sh.S,
+                                                         sh.padW, sh.padH, 1, (unsigned)(sh.C / 16), cp, nonfinite);
+        tc_to_hwcn_split_kernel<true><<<tb_y, 256, 0, st>>>(chk, y_hi, y_lo, sh.N, sh.K, HWp, nonfinite);
+        tc_to_hwcn_split_kernel<false><<<tb_d, 256, 0, st>>>(oth, d_hi, d_lo, sh.N, sh.C, HW, nonfinite);
+    }
+    note_launch(cp ? 3 : 2);
+    CUtensorMap ahi, alo, bhi, blo;
+    // pixel-major [NB][H][W][C][16] = 5-D (16, C, W, H, NB); boxes = one pixel's channel tile
+    const int dY5[5] = {16, sh.K, sh.Wp, sh.Hp, NB}, dD5[5] = {16, sh.C, sh.W, sh.H, NB};
+    const int bA[5] = {16, TC_BM, 1, 1, 1}, bB[5] = {16, cw, 1, 1, 1};
+    if (!make_map5(&ahi, y_hi, dY5, bA) || !make_map5(&alo, y_lo, dY5, bA) || !make_map5(&bhi, d_hi, dD5, bB) ||
+        !make_map5(&blo, d_lo, dD5, bB)) {
+        cudaFreeAsync(scratch, st);
+        return cudaErrorInvalidValue;
+    }
+    unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
+    if (BN == 256)
+        e = launch_bww_bn<256>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+    else if (BN == 192)
+        e = launch_bww_bn<192>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+    else if (BN == 128)
+        e = launch_bww_bn<128>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+    else
+        e = launch_bww_bn<64>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+    if (e == cudaSuccess) {
+        tc_bww_reduce_kernel<<<148 * 4, 256, 0, st>>>(part, dst, g.splits, sh.K, sh.C, sh.R, sh.S, nonfinite);
+        note_launch();
+        e = cudaGetLastError();
+    }
+    // non-finite operands: the FFMA BWW with the reference's exact skip semantics
+    if (e == cudaSuccess) e = launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, nonfinite, 1);
     cudaFreeAsync(scratch, st);
     return e;
 }

@@ -403,7 +403,9 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
 
 // Sum the splits in fixed order and scatter into FilterKCRSblk (K, C).
 template <bool CHECK_INPUT>
-__global__ void bww_tile_reduce(DevShape sh, const float* __restrict__ partial, int splits, float* __restrict__ dst) {
+__global__ void bww_tile_reduce(DevShape sh, const float* __restrict__ partial, int splits, float* __restrict__ dst,
+                                const int* __restrict__ sel = nullptr, int want = 0) {
+    if (sel != nullptr && __ldg(sel) != want) return;
     const int TAPS = sh.R * sh.S;
     const int Lc = CHECK_INPUT ? sh.K : sh.C, Mc = CHECK_INPUT ? sh.C : sh.K;
     const size_t E = (size_t)Mc * TAPS * Lc;
@@ -425,7 +427,8 @@ __global__ void bww_tile_reduce(DevShape sh, const float* __restrict__ partial, 
 // device (the other exits at entry), no host synchronisation.
 template <bool CI, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, bool JTSEL = false>
 static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* chk, const float* oth,
-                                  float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
+                                  float* dst, unsigned long long* exec_ctr, cudaStream_t st,
+                                  const int* xsel = nullptr, int xwant = 0) {
     using G = BwwGeom<CI, KK, CB, NWC, TH, TW, R, S, STR>;
     const int Lc = CI ? sh.K : sh.C, Mc = CI ? sh.C : sh.K;
     const long items = (long)((sh.N + 15) / 16) * ((sh.Wp + TW - 1) / TW) * ((sh.Hp + TH - 1) / TH);
@@ -456,14 +459,14 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
         auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, true>
                            : bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        kern<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, nullptr, 0);
+        kern<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, xsel, xwant);
         note_launch();
     }
     e = cudaGetLastError();
     if (e == cudaSuccess) {
         unsigned rb = (unsigned)((E + 255) / 256);
         if (rb > 148 * 8) rb = 148 * 8;
-        bww_tile_reduce<CI><<<rb, 256, 0, st>>>(sh, partial, (int)splits, dst);
+        bww_tile_reduce<CI><<<rb, 256, 0, st>>>(sh, partial, (int)splits, dst, xsel, xwant);
         note_launch();
         e = cudaGetLastError();
     }
@@ -553,6 +556,28 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
     }
     if (kk4) SPC_B(false, 4, 4, 4, 4, 8, 1, 2);
     SPC_B(false, 2, 4, 4, 4, 8, 1, 2);
+#undef SPC_B
+}
+
+// The default stride-1 configurations gated on a device word (*sel == want):
+// the exact FFMA BWW behind the tensor-core variant for Inf/NaN operands.
+cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& sh, const float* chk,
+                                 const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st,
+                                 const int* sel, int want) {
+    const bool kk4 = (check_input ? sh.K : sh.C) % 128 == 0;
+#define SPC_B(CI, KK, CB, NWC, TH, TW, R) \
+    return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, 1>(sparse, sh, chk, oth, dst, exec_ctr, st, sel, want)
+    if (check_input) {
+        if (sh.R == 3) {
+            if (kk4) SPC_B(true, 4, 1, 8, 7, 4, 3);
+            SPC_B(true, 2, 2, 4, 4, 7, 3);
+        }
+        if (kk4) SPC_B(true, 4, 4, 4, 4, 8, 1);
+        SPC_B(true, 2, 4, 4, 4, 8, 1);
+    }
+    if (sh.R == 3) SPC_B(false, 2, 1, 8, 4, 7, 3);
+    if (kk4) SPC_B(false, 4, 4, 4, 4, 8, 1);
+    SPC_B(false, 2, 4, 4, 4, 8, 1);
 #undef SPC_B
 }
 

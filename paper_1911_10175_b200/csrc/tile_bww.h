@@ -9,4 +9,7 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
                             float* dst, unsigned long long* exec_ctr, cudaStream_t st);
 cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, const DevShape& sh, const float* chk,
                                     const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st);
+cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& sh, const float* chk,
+                                 const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st,
+                                 const int* sel, int want);
 }  // namespace spc

@@ -126,3 +126,63 @@ def test_tc_fused_epilogue(sp):
     f32, tc = outs
     assert np.array_equal(f32 == 0, tc == 0) or np.mean((f32 == 0) != (tc == 0)) < 1e-4
     assert O.max_abs_rel(tc, f32) <= TC_TOL
+
+
+BWW_SHAPES = [
+    (3, 64, 128, 13, 9, 3, 3),      # ragged 16-image block, odd extents
+    (16, 128, 256, 28, 28, 3, 3),
+    (4, 256, 128, 14, 14, 3, 3),
+    (2, 512, 512, 7, 7, 3, 3),
+    (20, 64, 64, 30, 17, 3, 3),
+    (8, 128, 256, 14, 14, 1, 1),
+]
+
+
+@pytest.mark.parametrize("shape", BWW_SHAPES)
+@pytest.mark.parametrize("check", [0, 1])
+def test_tc_bww_matches_oracle(sp, shape, check):
+    rng = np.random.default_rng((hash(shape) + check) & 0xFFFF)
+    N, C, K, H, W, R, S = shape
+    sh = sp.ConvShape.make(N, C, K, H, W, R, S, 1, 1)
+    t = sh.astuple()
+    d = _gauss_relu(rng, (N, C, H, W), 0.6)
+    dy = _gauss_relu(rng, (N, K, sh.out_h(), sh.out_w()), 0.5)
+    ref = O.dense(2, t, d, dy)
+    if check == 0:
+        ba, bb = sp.pack_act_chwnn(d, V), sp.pack_act_nchwc(dy, V)
+    else:
+        ba, bb = sp.pack_act_nchwc(d, V), sp.pack_act_chwnn(dy, V)
+    ba, bb = ba.to("cuda"), bb.to("cuda")
+    pl = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck(check))
+    with sp.math_mode(sp.Math.tf32x3):
+        res = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse)
+        dres = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.dense)
+    got = sp.unpack(res.out).cpu().numpy()
+    err = O.max_abs_rel(got, ref)
+    assert err <= TC_TOL, (shape, check, err)
+    want = O.expected_counts(t, O.plan(t, 2, V, 30, check), d if check == 0 else dy)
+    assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+    assert res.counters.checked_vectors == want["checked_vectors"]
+    assert np.array_equal(sp.unpack(dres.out).cpu().numpy(), got)
+    assert dres.counters.executed_vector_fmas == want["dense_total"]
+
+
+def test_tc_bww_nonfinite_takes_exact_path(sp):
+    rng = np.random.default_rng(21)
+    sh = sp.ConvShape.make(4, 64, 128, 10, 10, 3, 3, 1, 1)
+    d = _gauss_relu(rng, (4, 64, 10, 10), 0.5)
+    dy = _gauss_relu(rng, (4, 128, 10, 10), 0.5)
+    dy[1, 5, 3, 3] = np.inf
+    d[2, 7, 4, 4] = np.nan
+    ba, bb = sp.pack_act_chwnn(d, V).to("cuda"), sp.pack_act_nchwc(dy, V).to("cuda")
+    pl = sp.plan(sh, sp.Component.bww, V)
+    outs = []
+    for m in (sp.Math.fp32, sp.Math.tf32x3):
+        with sp.math_mode(m):
+            r = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse)
+            outs.append((sp.unpack(r.out).cpu().numpy(), r.counters.executed_vector_fmas))
+    (f32, c32), (tc, ctc) = outs
+    assert np.array_equal(np.isnan(tc), np.isnan(f32)) and np.array_equal(np.isinf(tc), np.isinf(f32))
+    fin = np.isfinite(f32)
+    assert np.array_equal(tc[fin], f32[fin])
+    assert ctc == c32
