@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tc", action="store_true", help="skip the 3xTF32 tensor-core variant")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -367,6 +368,8 @@ def main():
 
     # speedup vs the same kernels run dense (zero check off) at sparsity 0
     dense0 = dense_baseline(sp, wl, layers, dev, sptr, V)
+    # the optional 3xTF32 tensor-core variant on the same resident work
+    tc = None if args.no_tc else tf32x3_variant(args, sp, work, step, stream, ws, distributed)
 
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
@@ -376,6 +379,8 @@ def main():
         "clocks": clocks.summary(), "roofline": roofline, "sweep": breakdown,
         "dense_mode_at_s0": dense0,
     }
+    if tc is not None:
+        out["tf32x3_variant"] = tc
     if rank == 0 and ws == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, layers)
     if not args.no_e2e:
@@ -385,6 +390,68 @@ def main():
     if distributed:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def tf32x3_variant(args, sp, work, step, stream, ws, distributed):
+    """The same step with spc_set_math(SPC_MATH_TF32X3): FWD/BWI/BWW on the
+    tcgen05 tensor cores with 3xTF32 split products.  A
+    separately stated tolerance; reported beside -- not instead of -- the FP32
+    FFMA headline."""
+    import numpy as np
+    import torch
+    prev = sp.set_math(sp.Math.tf32x3)
+    try:
+        step()  # warm-up (scratch pools, tensor maps)
+        torch.cuda.synchronize()
+        if distributed:
+            import torch.distributed as dist
+            dist.barrier()
+        events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in work]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(events)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    finally:
+        sp.set_math(prev)
+    total_ms = e0.elapsed_time(e1)
+    if distributed:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    per = np.array([a.elapsed_time(b) for a, b in events])
+    flops_step = sum(w[4] for w in work)
+    sweep = {}
+    for idx, (s, li, name, pp, fl) in enumerate(work):
+        d = sweep.setdefault(f"{s:.1f}", {}).setdefault(name, [0.0, 0.0])
+        d[0] += fl
+        d[1] += per[idx]
+    fam = {n: [sum(w[4] for w in work if w[2] == n), sum(per[i] for i, w in enumerate(work) if w[2] == n)]
+           for n in PASSES}
+    dom = max(fam, key=lambda n: fam[n][1])
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        tf32_peak, peak_src = peaks["bf16_tflops"] / 2.0, "MEASURED_PEAKS.json bf16_tflops / 2 (tf32 = half bf16 rate)"
+    except Exception:
+        tf32_peak, peak_src = 1100.0, "B200_PROFILING.md nominal dense tf32 1.1 PFLOP/s (fallback)"
+    mma_tflops = 3.0 * fam[dom][0] / (fam[dom][1] * 1e-3) / 1e12  # three tf32 products per fp32 product
+    return {
+        "math": "3xTF32 split products (hi*hi + hi*lo + lo*hi), fp32 accumulation in TMEM drained to fp32 "
+                "registers every 8 pipeline stages; spc_set_math(SPC_MATH_TF32X3)",
+        "tolerance": "max|got-ref|/max|ref| <= 1e-5 vs the 64-bit oracle (tests/test_gpu_tc.py); measured "
+                     "0.5e-6 - 1.4e-6 (the reference CPU fp32 kernels: 0.4e-6 - 1.0e-6)",
+        "value": round(ws * flops_step / (ms_step * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+        "ms_per_step": round(ms_step, 3),
+        "sweep": {s: {n: {"dense_equiv_gflops": round(f / ms / 1e6, 1), "ms": round(ms, 3)}
+                      for n, (f, ms) in d.items()} for s, d in sweep.items()},
+        "roofline": {"bound": "tensor", "kernel": f"{dom} tcgen05 kernel", "achieved": round(mma_tflops, 1),
+                     "peak": round(tf32_peak, 1), "unit": "TFLOP/s", "frac": round(mma_tflops / tf32_peak, 4),
+                     "basis": "issued tf32 MMA FLOPs = 3 x dense-equiv FLOPs (padding rows not counted) / "
+                              "CUDA-event pass durations (prep + GEMM + reduce); peak = " + peak_src},
+    }
 
 
 def ffma_peak(sp, dev, sptr):
