@@ -71,10 +71,11 @@ struct TcGeo {
     int sgn;           // +1 FWD (src = out + tap - pad), -1 BWI (src = out + pad - tap)
     int padW, padH;
     int seg;           // pipeline stages per TMEM accumulation segment
+    int N, ntiles;     // images; tiles = N * tiles_x * tiles_y * (Co / BN)
     size_t out_img;    // floats per output image
 };
 
-template <int BN>
+template <int BN, int ST>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
                    const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -88,28 +89,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int HALF = BN / 2;  // accumulator columns per epilogue thread
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_ST * STAGE);  // full[ST] empty[ST] tfull[2] tempty[2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_ST + 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);  // full[ST] empty[ST] tfull[2] tempty[2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x;
-    const int img = tile / (g.tiles_x * g.tiles_y);
-    const int trem = tile - img * g.tiles_x * g.tiles_y;
-    const int ty = trem / g.tiles_x, tx = trem - ty * g.tiles_x;
-    const int x0 = tx * g.bw, y0 = ty * g.bh;
-    const int n0 = blockIdx.y * BN;
-    const int niter = g.RB * g.R * g.S;
-    const int D = g.seg;  // stages per accumulation segment
-    const int nseg = (niter + D - 1) / D;
+    // persistent: this CTA runs tiles blockIdx.x, + gridDim.x, ...; tile t =
+    // (n tile, image, box row, box column), n tile slowest so the CTAs in
+    // flight share one filter slice in L2
+    const int txy = g.tiles_x * g.tiles_y;
+    const int ntiles = g.ntiles;
+    const int niter = g.RB * g.R * g.S;       // pipeline stages per tile
+    const int D = g.seg;                      // stages per accumulation segment
+    const int nseg = (niter + D - 1) / D;     // segments per tile
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (TC_ST + s); };
-    auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * TC_ST + b); };
-    auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * TC_ST + 2 + b); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * ST + b); };
+    auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * ST + 2 + b); };
+    auto tile_coords = [&](int t, int& img, int& x0, int& y0, int& n0) {
+        const int nt = t / (g.N * txy);
+        int r = t - nt * g.N * txy;
+        img = r / txy;
+        r -= img * txy;
+        const int ty = r / g.tiles_x;
+        x0 = (r - ty * g.tiles_x) * g.bw;
+        y0 = ty * g.bh;
+        n0 = nt * BN;
+    };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_ST; ++s) {
+        for (int s = 0; s < ST; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
@@ -119,7 +129,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (blockIdx.x == 0 && blockIdx.y == 0 && cnt_tmp && exec_ctr) atomicAdd(exec_ctr, *cnt_tmp);
+        if (blockIdx.x == 0 && cnt_tmp && exec_ctr) atomicAdd(exec_ctr, *cnt_tmp);
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -138,23 +148,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
-            int rb = 0, v = 0, u = 0;
-            for (int it = 0; it < niter; ++it) {
-                const int s = it % TC_ST;
-                if (it >= TC_ST) mbar_wait(empty_bar(s), ((it / TC_ST) - 1) & 1);
-                const uint32_t st = sbase + s * STAGE;
-                mbar_expect_tx(full_bar(s), STAGE);
-                const int sx = x0 + g.sgn * (u - g.padW), sy = y0 + g.sgn * (v - g.padH);
-                tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
-                tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
-                const int brow = (v * g.R + u) * g.RB + rb;
-                tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
-                tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
-                if (++u == g.R) {
-                    u = 0;
-                    if (++v == g.S) {
-                        v = 0;
-                        ++rb;
+            int gi = 0;  // stage counter across this CTA's tiles (the smem ring continues)
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int img, x0, y0, n0;
+                tile_coords(t, img, x0, y0, n0);
+                int rb = 0, v = 0, u = 0;
+                for (int it = 0; it < niter; ++it, ++gi) {
+                    const int s = gi % ST;
+                    if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
+                    const uint32_t st = sbase + s * STAGE;
+                    mbar_expect_tx(full_bar(s), STAGE);
+                    const int sx = x0 + g.sgn * (u - g.padW), sy = y0 + g.sgn * (v - g.padH);
+                    tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
+                    tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
+                    const int brow = (v * g.R + u) * g.RB + rb;
+                    tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
+                    tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
+                    if (++u == g.R) {
+                        u = 0;
+                        if (++v == g.S) {
+                            v = 0;
+                            ++rb;
+                        }
                     }
                 }
             }
@@ -162,27 +177,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t idesc = tf32_idesc<BN>();
-            for (int it = 0; it < niter; ++it) {
-                const int seg = it / D, buf = seg & 1;
-                const bool first = it - seg * D == 0;
-                if (first && seg >= 2) mbar_wait(tempty_bar(buf), ((seg >> 1) - 1) & 1);
-                const int s = it % TC_ST;
-                mbar_wait(full_bar(s), (it / TC_ST) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t st = sbase + s * STAGE;
-                const uint32_t tm = tmem + buf * BN;
+            int gi = 0, gseg = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int it = 0; it < niter; ++it, ++gi) {
+                    const int ls = it / D;  // segment within the tile
+                    const bool first = it - ls * D == 0;
+                    const int sg = gseg + ls, buf = sg & 1;
+                    if (first && sg >= 2) mbar_wait(tempty_bar(buf), ((sg >> 1) - 1) & 1);
+                    const int s = gi % ST;
+                    mbar_wait(full_bar(s), (gi / ST) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t st = sbase + s * STAGE;
+                    const uint32_t tm = tmem + buf * BN;
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {  // two K=8 steps per 16-channel block (32 bytes each)
-                    const uint64_t ahi = sw64_desc(st + 32 * k);
-                    const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
-                    const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
-                    const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + 32 * k);
-                    umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
-                    umma_tf32(tm, ahi, blo, idesc, 1u);
-                    umma_tf32(tm, ahi, bhi, idesc, 1u);
+                    for (int k = 0; k < 2; ++k) {  // two K=8 steps per 16-channel block (32 bytes each)
+                        const uint64_t ahi = sw64_desc(st + 32 * k);
+                        const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
+                        const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
+                        const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + 32 * k);
+                        umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
+                        umma_tf32(tm, ahi, blo, idesc, 1u);
+                        umma_tf32(tm, ahi, bhi, idesc, 1u);
+                    }
+                    umma_commit(empty_bar(s));
+                    if (it - ls * D == D - 1 || it == niter - 1) umma_commit(tfull_bar(buf));
                 }
-                umma_commit(empty_bar(s));
-                if (it - seg * D == D - 1 || it == niter - 1) umma_commit(tfull_bar(buf));
+                gseg += nseg;
             }
         }
         __syncwarp();
@@ -191,48 +211,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // accessible lanes) = output pixels 32q..32q+31; column half h.
         // Each segment's partial sums are drained into fp32 registers
         // (round-to-nearest adds), which bounds the length of the tensor
-        // core's truncating accumulation chain.
+        // core's truncating accumulation chain; the store of
+        // a tile overlaps the next tile's MMAs.
         const int q = warp & 3, h = (warp - 2) >> 2;
         const int m = q * 32 + lane;
         const int py = m / g.bw, px = m - py * g.bw;
-        const int y = y0 + py, x = x0 + px;
-        float acc[HALF];
-#pragma unroll
-        for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        for (int seg = 0; seg < nseg; ++seg) {
-            const int buf = seg & 1;
-            mbar_wait_sleep(tfull_bar(buf), (seg >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const size_t plane = (size_t)g.Ho * g.Wo * 16;
+        int gseg = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int img, x0, y0, n0;
+            tile_coords(t, img, x0, y0, n0);
+            float acc[HALF];
 #pragma unroll
-            for (int j = 0; j < HALF / 16; ++j) {
-                float v[16];
-                tmem_ld16(tmem + lane_off + buf * BN + h * HALF + 16 * j, v);
+            for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
+            for (int ls = 0; ls < nseg; ++ls) {
+                const int sg = gseg + ls, buf = sg & 1;
+                mbar_wait_sleep(tfull_bar(buf), (sg >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int e = 0; e < 16; ++e) acc[16 * j + e] += v[e];
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar(buf)) : "memory");
-        }
-        if (y < g.Ho && x < g.Wo) {
-            const size_t plane = (size_t)g.Ho * g.Wo * 16;
-            float* out = dst + (size_t)img * g.out_img + ((size_t)y * g.Wo + x) * 16;
+                for (int j = 0; j < HALF / 16; ++j) {
+                    float v[16];
+                    tmem_ld16(tmem + lane_off + buf * BN + h * HALF + 16 * j, v);
 #pragma unroll
-            for (int j = 0; j < HALF / 16; ++j) {
-                const int kb = ((n0 + h * HALF) >> 4) + j;
-                float* o = out + (size_t)kb * plane;
-                float v[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = acc[16 * j + e];
-                if (epi.active()) {
-                    const size_t base = (size_t)(o - dst);
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = epi.apply(v[e], base + e);
+                    for (int e = 0; e < 16; ++e) acc[16 * j + e] += v[e];
                 }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty_bar(buf));
+            }
+            gseg += nseg;
+            const int y = y0 + py, x = x0 + px;
+            if (y < g.Ho && x < g.Wo) {
+                float* out = dst + (size_t)img * g.out_img + ((size_t)y * g.Wo + x) * 16;
 #pragma unroll
-                for (int e = 0; e < 16; e += 4)
-                    *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                for (int j = 0; j < HALF / 16; ++j) {
+                    const int kb = ((n0 + h * HALF) >> 4) + j;
+                    float* o = out + (size_t)kb * plane;
+                    float v[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = acc[16 * j + e];
+                    if (epi.active()) {
+                        const size_t base = (size_t)(o - dst);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = epi.apply(v[e], base + e);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; e += 4)
+                        *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                }
             }
         }
     }
@@ -240,7 +267,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN)) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN))
+                     : "memory");
     }
 }
 
@@ -349,15 +377,29 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
                       const CUtensorMap& mblo, const TcGeo& g, int N, float* dst, const int* nonfinite,
                       const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st) {
     constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * BN * 64;
-    const size_t smem = TC_ST * STAGE + 1024 + 256;
+    // 4 stages (3 stages at BN = 128 with two CTAs per SM measured 1-3% slower)
+    constexpr int ST = 4;
+    const size_t smem = ST * STAGE + 1024 + 256;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid((unsigned)(N * g.tiles_x * g.tiles_y), (unsigned)(g.Co / BN));
-    tc_conv_kernel<BN><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, g, dst, nonfinite, cnt, exec_ctr, epi);
+    TcGeo gg = g;
+    gg.N = N;
+    gg.ntiles = N * g.tiles_x * g.tiles_y * (g.Co / BN);
+    // persistent CTAs: as many as fit per SM (2 for BN <= 128: their
+    // prologues / stores overlap each other's main loops), or fewer tiles
+    // (measured, VGG conv1_2 FWD at BN = 64: 1 CTA/SM 75, 2 CTAs/SM 117 TFLOP/s)
+    const int per_sm = (int)((228u * 1024u) / (smem + 1024u)) >= 2 ? 2 : 1;
+    static const int persist_env = std::getenv("SPC_TC_CTAS") ? std::atoi(std::getenv("SPC_TC_CTAS")) : 0;
+    int ctas = persist_env > 0 ? persist_env : 148 * per_sm;
+    if (ctas > gg.ntiles) ctas = gg.ntiles;
+    dim3 grid((unsigned)ctas);
+    tc_conv_kernel<BN, ST><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt, exec_ctr, epi);
     note_launch();
     return cudaGetLastError();
 }
@@ -625,7 +667,9 @@ cudaError_t launch_bww_bn(const CUtensorMap& ahi, const CUtensorMap& alo, const 
                           const CUtensorMap& blo, const TcBwwGeo& g, float* partial, const int* nonfinite,
                           const unsigned long long* cnt, unsigned long long* exec_ctr, cudaStream_t st) {
     constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * BN * 64;
-    const size_t smem = TC_ST * STAGE + 1024 + 256;
+    // 4 stages (3 stages at BN = 128 with two CTAs per SM measured 1-3% slower)
+    constexpr int ST = 4;
+    const size_t smem = ST * STAGE + 1024 + 256;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(tc_bww_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

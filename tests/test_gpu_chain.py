@@ -37,7 +37,21 @@ def _fma(a, alpha, add):  # fmaf(a, alpha, add) per element (exact in float64 he
 def test_chain_step_matches_oracle_pass_by_pass(mode):
     blocks = CH.resnet50_blocks(H=10, W=10, cin=32, stages=((16, 1), (32, 2)))
     assert [b.proj for b in blocks] == [True, True, False]
-    ch = CH.FixupChain(3, blocks, scale=0.5, seed=7, mode=mode, x_sparsity=0.6)
+    _check_chain(CH.FixupChain(3, blocks, scale=0.5, seed=7, mode=mode, x_sparsity=0.6), blocks)
+
+
+def test_chain_step_tf32x3_matches_oracle_pass_by_pass():
+    """The same step with the 3xTF32 tensor-core variant (64-channel multiples,
+    so its 1x1 / 3x3 stride-1 passes run on tcgen05; stride-2 passes stay FP32)."""
+    blocks = CH.resnet50_blocks(H=8, W=8, cin=64, stages=((64, 1), (128, 2)))
+    launches = sp.launch_count()
+    with sp.math_mode(sp.Math.tf32x3):
+        _check_chain(CH.FixupChain(3, blocks, scale=0.5, seed=11, mode=sp.RunMode.sparse, x_sparsity=0.6),
+                     blocks)
+    assert sp.launch_count() > launches
+
+
+def _check_chain(ch, blocks):
     ch.set_upstream()
     ch.step()
     torch.cuda.synchronize()

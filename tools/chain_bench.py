@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--mode", default="sparse", choices=["sparse", "dense"])
     ap.add_argument("--x-sparsity", type=float, default=0.7)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--math", default="fp32", choices=["fp32", "tf32x3"])
     a = ap.parse_args()
 
     import torch
@@ -48,6 +49,7 @@ def main():
     distributed = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
+    sp.set_math(sp.Math[a.math])
     _, n_local = shard_range(a.batch, ws, rank)
     t0 = time.time()
     ar = GradAllreduce(device=dev) if distributed else None
