@@ -75,7 +75,7 @@ struct TcGeo {
     size_t out_img;    // floats per output image
 };
 
-template <int BN, int ST>
+template <int BN, int ST, int KB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
                    const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -83,8 +83,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr,
                    Epi epi) {
     if (__ldg(nonfinite) != 0) return;  // the exact FFMA kernel runs instead
-    constexpr uint32_t A_BYTES = TC_BM * 64;
-    constexpr uint32_t B_BYTES = BN * 64;
+    // a stage = KB 16-channel blocks of one tap: A = KB sub-tiles of 128 rows x
+    // 64 B (hi, then lo), B = KB sub-tiles of BN rows x 64 B (hi, then lo)
+    constexpr uint32_t A_BYTES = KB * TC_BM * 64;
+    constexpr uint32_t B_BYTES = KB * BN * 64;
     constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
     constexpr int HALF = BN / 2;  // accumulator columns per epilogue thread
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // flight share one filter slice in L2
     const int txy = g.tiles_x * g.tiles_y;
     const int ntiles = g.ntiles;
-    const int niter = g.RB * g.R * g.S;       // pipeline stages per tile
+    const int niter = (g.RB / KB) * g.R * g.S;  // pipeline stages per tile
     const int D = g.seg;                      // stages per accumulation segment
     const int nseg = (niter + D - 1) / D;     // segments per tile
     const uint32_t sbase = smem_u32(smem);
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         u = 0;
                         if (++v == g.S) {
                             v = 0;
-                            ++rb;
+                            rb += KB;
                         }
                     }
                 }
@@ -190,11 +192,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const uint32_t st = sbase + s * STAGE;
                     const uint32_t tm = tmem + buf * BN;
 #pragma unroll
-                    for (int k = 0; k < 2; ++k) {  // two K=8 steps per 16-channel block (32 bytes each)
-                        const uint64_t ahi = sw64_desc(st + 32 * k);
-                        const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
-                        const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
-                        const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + 32 * k);
+                    for (int k = 0; k < 2 * KB; ++k) {  // two K=8 steps (32 bytes) per 16-channel block
+                        const uint32_t ao = (k >> 1) * (TC_BM * 64) + 32 * (k & 1);
+                        const uint32_t bo = (k >> 1) * (BN * 64) + 32 * (k & 1);
+                        const uint64_t ahi = sw64_desc(st + ao);
+                        const uint64_t alo = sw64_desc(st + A_BYTES + ao);
+                        const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + bo);
+                        const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + bo);
                         umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
                         umma_tf32(tm, ahi, blo, idesc, 1u);
                         umma_tf32(tm, ahi, bhi, idesc, 1u);
@@ -347,11 +351,11 @@ __global__ void tc_zero_kernel(int* flag, unsigned long long* cnt) {
 }
 
 // ---------------------------------------------------------------- host
-// K-major filter copy [taps*RB][Co][16], box = 16 x bn x 1.
-bool make_filter_map(CUtensorMap* m, const float* p, int rows, int Co, int bn) {
+// K-major filter copy [taps*RB][Co][16], box = 16 x bn x kb.
+bool make_filter_map(CUtensorMap* m, const float* p, int rows, int Co, int bn, int kb = 1) {
     cuuint64_t dims[3] = {16, (cuuint64_t)Co, (cuuint64_t)rows};
     cuuint64_t strides[2] = {64, (cuuint64_t)Co * 64};
-    cuuint32_t box[3] = {16, (cuuint32_t)bn, 1};
+    cuuint32_t box[3] = {16, (cuuint32_t)bn, (cuuint32_t)kb};
     cuuint32_t es[3] = {1, 1, 1};
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -372,19 +376,20 @@ void choose_box(int Ho, int Wo, int* bw, int* bh) {
     }
 }
 
-template <int BN>
+template <int BN, int KB>
 cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUtensorMap& mbhi,
                       const CUtensorMap& mblo, const TcGeo& g, int N, float* dst, const int* nonfinite,
                       const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st) {
-    constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * BN * 64;
-    // 4 stages (3 stages at BN = 128 with two CTAs per SM measured 1-3% slower)
-    constexpr int ST = 4;
+    constexpr size_t STAGE = KB * (2 * TC_BM * 64 + 2 * BN * 64);
+    // 4 stages (3 stages at BN = 128 with two CTAs per SM measured 1-3% slower);
+    // 2-block stages: as many stages as fit 200 KB
+    constexpr int ST = KB == 1 ? 4 : (int)((200 * 1024) / STAGE);
     const size_t smem = ST * STAGE + 1024 + 256;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -399,7 +404,7 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     int ctas = persist_env > 0 ? persist_env : 148 * per_sm;
     if (ctas > gg.ntiles) ctas = gg.ntiles;
     dim3 grid((unsigned)ctas);
-    tc_conv_kernel<BN, ST><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt, exec_ctr, epi);
+    tc_conv_kernel<BN, ST, KB><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt, exec_ctr, epi);
     note_launch();
     return cudaGetLastError();
 }
@@ -667,9 +672,7 @@ cudaError_t launch_bww_bn(const CUtensorMap& ahi, const CUtensorMap& alo, const 
                           const CUtensorMap& blo, const TcBwwGeo& g, float* partial, const int* nonfinite,
                           const unsigned long long* cnt, unsigned long long* exec_ctr, cudaStream_t st) {
     constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * BN * 64;
-    // 4 stages (3 stages at BN = 128 with two CTAs per SM measured 1-3% slower)
-    constexpr int ST = 4;
-    const size_t smem = ST * STAGE + 1024 + 256;
+    const size_t smem = TC_ST * STAGE + 1024 + 256;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(tc_bww_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -740,21 +743,30 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     g.seg = seg_env > 0 ? seg_env : 8;  // error 1.2-1.4e-6 measured
 
     CUtensorMap mhi, mlo, mbhi, mblo;
+    // N tile 256 when Co allows (128-wide tiles to fill the last round of
+    // persistent CTAs measured slower: VGG conv3_2 185 -> 156, conv4 170 -> 155)
     const int bn = Co % 256 == 0 ? 256 : (Co % 128 == 0 ? 128 : 64);
-    if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, 1) ||
-        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, 1) ||
-        !make_filter_map(&mbhi, bhi, taps * (Cr / 16), Co, bn) ||
-        !make_filter_map(&mblo, blo, taps * (Cr / 16), Co, bn)) {
+    // BN = 128: two 16-channel blocks per pipeline stage (K = 32: twice the
+    // MMAs per barrier round trip; measured VGG conv2_2 140 -> 180 TF/s).  BN =
+    // 64 keeps one block per stage and two CTAs per SM (2-block stages there:
+    // 117 -> 103), BN = 256 one (a 96 KB stage would leave 2 stages).
+    static const int kb_env = std::getenv("SPC_TC_KB") ? std::atoi(std::getenv("SPC_TC_KB")) : 0;
+    const int kb = (kb_env == 1 || bn != 128 || (Cr / 16) % 2) ? 1 : 2;
+    if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb) ||
+        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb) ||
+        !make_filter_map(&mbhi, bhi, taps * (Cr / 16), Co, bn, kb) ||
+        !make_filter_map(&mblo, blo, taps * (Cr / 16), Co, bn, kb)) {
         cudaFreeAsync(scratch, st);
         return cudaErrorInvalidValue;
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
     if (bn == 256)
-        e = launch_bn<256>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
+        e = launch_bn<256, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
     else if (bn == 128)
-        e = launch_bn<128>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
+        e = kb == 2 ? launch_bn<128, 2>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st)
+                    : launch_bn<128, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
     else
-        e = launch_bn<64>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
+        e = launch_bn<64, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
     // non-finite source or filter: the FFMA tile kernel with the reference's exact skip semantics
     if (e == cudaSuccess) e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
     cudaFreeAsync(scratch, st);
