@@ -76,12 +76,12 @@ struct TcGeo {
 };
 
 template <int BN, int ST, int KB>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two CTAs per SM (<= 96 registers)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
                    const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                    TcGeo g, float* __restrict__ dst, const int* __restrict__ nonfinite,
                    const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr,
-                   Epi epi) {
+                   Epi epi, const uint8_t* __restrict__ zflag) {
     if (__ldg(nonfinite) != 0) return;  // the exact FFMA kernel runs instead
     // a stage = KB 16-channel blocks of one tap: A = KB sub-tiles of 128 rows x
     // 64 B (hi, then lo), B = KB sub-tiles of BN rows x 64 B (hi, then lo)
@@ -100,20 +100,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // flight share one filter slice in L2
     const int txy = g.tiles_x * g.tiles_y;
     const int ntiles = g.ntiles;
-    const int niter = (g.RB / KB) * g.R * g.S;  // pipeline stages per tile
+    const int NG = g.RB / KB;                 // channel-block groups (one per tap sweep)
+    const int taps = g.R * g.S;
     const int D = g.seg;                      // stages per accumulation segment
-    const int nseg = (niter + D - 1) / D;     // segments per tile
+    // all-zero tile skipping (sparse mode): zflag[img][group][tile] = 0 when the
+    // tile's source box (all taps) is zero in the group's channels; every role
+    // reads the same flags, so the skipped stages never enter the pipeline
+    // a tile's flags as a bit mask (NG <= 64, host-checked), loaded once per
+    // tile by each role: no flag load on the MMA issue path
+    auto live_mask = [&](int img, int tt) {
+        if (zflag == nullptr) return ~0ull;
+        unsigned long long m = 0;
+        for (int grp = 0; grp < NG; ++grp)
+            m |= (unsigned long long)(__ldg(zflag + ((size_t)img * NG + grp) * txy + tt) != 0) << grp;
+        return m;
+    };
+    // Segments are fixed runs of D stages of the FULL stage sequence (dense
+    // order), so skipping leaves every segment's summation grouping -- and the
+    // result -- bitwise equal to dense mode; a segment with no live stage is
+    // skipped by the MMA issuer and the epilogue alike.
+    const int nstage = NG * taps;
+    const int nseg = (nstage + D - 1) / D;
+    auto seg_live = [&](unsigned long long lm, int ls) {
+        const int g0 = (ls * D) / taps, g1 = (min(ls * D + D, nstage) - 1) / taps;
+        const unsigned long long span = (g1 - g0 == 63) ? ~0ull : ((2ull << (g1 - g0)) - 1) << g0;
+        return (lm & span) != 0;
+    };
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
     auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * ST + b); };
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * ST + 2 + b); };
-    auto tile_coords = [&](int t, int& img, int& x0, int& y0, int& n0) {
+    auto tile_coords = [&](int t, int& img, int& x0, int& y0, int& n0, int& tt) {
         const int nt = t / (g.N * txy);
         int r = t - nt * g.N * txy;
         img = r / txy;
         r -= img * txy;
+        tt = r;
         const int ty = r / g.tiles_x;
         x0 = (r - ty * g.tiles_x) * g.bw;
         y0 = ty * g.bh;
@@ -152,27 +176,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
             int gi = 0;  // stage counter across this CTA's tiles (the smem ring continues)
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int img, x0, y0, n0;
-                tile_coords(t, img, x0, y0, n0);
-                int rb = 0, v = 0, u = 0;
-                for (int it = 0; it < niter; ++it, ++gi) {
-                    const int s = gi % ST;
-                    if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
-                    const uint32_t st = sbase + s * STAGE;
-                    mbar_expect_tx(full_bar(s), STAGE);
-                    const int sx = x0 + g.sgn * (u - g.padW), sy = y0 + g.sgn * (v - g.padH);
-                    tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
-                    tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
-                    const int brow = (v * g.R + u) * g.RB + rb;
-                    tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
-                    tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
-                    if (++u == g.R) {
-                        u = 0;
-                        if (++v == g.S) {
-                            v = 0;
-                            rb += KB;
+                int img, x0, y0, n0, tt;
+                tile_coords(t, img, x0, y0, n0, tt);
+                const unsigned long long lm = live_mask(img, tt);
+                for (int grp = 0; grp < NG; ++grp) {
+                    if (!((lm >> grp) & 1ull)) continue;
+                    const int rb = grp * KB;
+                    for (int v = 0; v < g.S; ++v)
+                        for (int u = 0; u < g.R; ++u, ++gi) {
+                            const int s = gi % ST;
+                            if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
+                            const uint32_t st = sbase + s * STAGE;
+                            mbar_expect_tx(full_bar(s), STAGE);
+                            const int sx = x0 + g.sgn * (u - g.padW), sy = y0 + g.sgn * (v - g.padH);
+                            tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
+                            tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
+                            const int brow = (v * g.R + u) * g.RB + rb;
+                            tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
+                            tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
                         }
-                    }
                 }
             }
         }
@@ -181,32 +203,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t idesc = tf32_idesc<BN>();
             int gi = 0, gseg = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                for (int it = 0; it < niter; ++it, ++gi) {
-                    const int ls = it / D;  // segment within the tile
-                    const bool first = it - ls * D == 0;
-                    const int sg = gseg + ls, buf = sg & 1;
-                    if (first && sg >= 2) mbar_wait(tempty_bar(buf), ((sg >> 1) - 1) & 1);
-                    const int s = gi % ST;
-                    mbar_wait(full_bar(s), (gi / ST) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t st = sbase + s * STAGE;
+                int img, x0, y0, n0, tt;
+                tile_coords(t, img, x0, y0, n0, tt);
+                const unsigned long long lm = live_mask(img, tt);
+                int ne = 0;  // live segments of this tile
+                for (int ls = 0; ls < nseg; ++ls) {
+                    if (!seg_live(lm, ls)) continue;
+                    const int sg = gseg + ne++, buf = sg & 1;
+                    if (sg >= 2) mbar_wait(tempty_bar(buf), ((sg >> 1) - 1) & 1);
                     const uint32_t tm = tmem + buf * BN;
+                    bool first = true;
+                    for (int it = ls * D; it < min(ls * D + D, nstage); ++it) {
+                        if (!((lm >> (it / taps)) & 1ull)) continue;
+                        const int s = gi % ST;
+                        mbar_wait(full_bar(s), (gi / ST) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint32_t st = sbase + s * STAGE;
 #pragma unroll
-                    for (int k = 0; k < 2 * KB; ++k) {  // two K=8 steps (32 bytes) per 16-channel block
-                        const uint32_t ao = (k >> 1) * (TC_BM * 64) + 32 * (k & 1);
-                        const uint32_t bo = (k >> 1) * (BN * 64) + 32 * (k & 1);
-                        const uint64_t ahi = sw64_desc(st + ao);
-                        const uint64_t alo = sw64_desc(st + A_BYTES + ao);
-                        const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + bo);
-                        const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + bo);
-                        umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
-                        umma_tf32(tm, ahi, blo, idesc, 1u);
-                        umma_tf32(tm, ahi, bhi, idesc, 1u);
+                        for (int k = 0; k < 2 * KB; ++k) {  // two K=8 steps (32 bytes) per 16-channel block
+                            const uint32_t ao = (k >> 1) * (TC_BM * 64) + 32 * (k & 1);
+                            const uint32_t bo = (k >> 1) * (BN * 64) + 32 * (k & 1);
+                            const uint64_t ahi = sw64_desc(st + ao);
+                            const uint64_t alo = sw64_desc(st + A_BYTES + ao);
+                            const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + bo);
+                            const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + bo);
+                            umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
+                            umma_tf32(tm, ahi, blo, idesc, 1u);
+                            umma_tf32(tm, ahi, bhi, idesc, 1u);
+                        }
+                        first = false;
+                        umma_commit(empty_bar(s));
+                        ++gi;
                     }
-                    umma_commit(empty_bar(s));
-                    if (it - ls * D == D - 1 || it == niter - 1) umma_commit(tfull_bar(buf));
+                    umma_commit(tfull_bar(buf));
                 }
-                gseg += nseg;
+                gseg += ne;
             }
         }
         __syncwarp();
@@ -224,13 +255,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const size_t plane = (size_t)g.Ho * g.Wo * 16;
         int gseg = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            int img, x0, y0, n0;
-            tile_coords(t, img, x0, y0, n0);
+            int img, x0, y0, n0, tt;
+            tile_coords(t, img, x0, y0, n0, tt);
             float acc[HALF];
 #pragma unroll
             for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
+            const unsigned long long lm = live_mask(img, tt);
+            int ne = 0;  // an all-zero tile has none: outputs = epi(0)
             for (int ls = 0; ls < nseg; ++ls) {
-                const int sg = gseg + ls, buf = sg & 1;
+                if (!seg_live(lm, ls)) continue;
+                const int sg = gseg + ne++, buf = sg & 1;
                 mbar_wait_sleep(tfull_bar(buf), (sg >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
@@ -244,7 +278,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(tempty_bar(buf));
             }
-            gseg += nseg;
+            gseg += ne;
             const int y = y0 + py, x = x0 + px;
             if (y < g.Ho && x < g.Wo) {
                 float* out = dst + (size_t)img * g.out_img + ((size_t)y * g.Wo + x) * 16;
@@ -345,6 +379,44 @@ __global__ void tc_split_filter_kernel(const float* __restrict__ f, float* __res
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(nonfinite, 1);
 }
 
+// zflag[img][group][tile] = 1 when the tile's source box -- the output box
+// widened by every tap's offset ([ylo, yhi] x [xlo, xhi]), clipped to the
+// image -- holds a nonzero in the group's KB 16-channel blocks, else 0 (all
+// the tile's MMAs for that group would multiply zeros).  One warp per flag.
+__global__ void tc_zero_tiles_kernel(const float* __restrict__ src, uint8_t* __restrict__ zflag, int N, int CB,
+                                     int KB, int Hs, int Ws, int tiles_x, int tiles_y, int bw, int bh, int ylo,
+                                     int yhi, int xlo, int xhi) {
+    const int NG = CB / KB, txy = tiles_x * tiles_y;
+    const long nflags = (long)N * NG * txy;
+    const int lane = threadIdx.x & 31;
+    for (long f = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5; f < nflags;
+         f += ((long)gridDim.x * blockDim.x) >> 5) {
+        const int tt = (int)(f % txy);
+        const int grp = (int)((f / txy) % NG);
+        const int img = (int)(f / ((long)txy * NG));
+        const int ty = tt / tiles_x, tx = tt - ty * tiles_x;
+        const int ya = max(ty * bh + ylo, 0), yb = min(ty * bh + bh - 1 + yhi, Hs - 1);
+        const int xa = max(tx * bw + xlo, 0), xb = min(tx * bw + bw - 1 + xhi, Ws - 1);
+        const int nx = xb - xa + 1, ny = yb - ya + 1;
+        bool nz = false;
+        if (nx > 0 && ny > 0) {
+            const long per_cb = (long)ny * nx * 4;  // float4s per channel block
+            for (long e = lane; e < per_cb * KB && !nz; e += 32) {
+                const int cb = grp * KB + (int)(e / per_cb);
+                long r = e % per_cb;
+                const int y = ya + (int)(r / (nx * 4));
+                r %= nx * 4;
+                const int x = xa + (int)(r >> 2), q = (int)(r & 3);
+                const float4 v = __ldg(reinterpret_cast<const float4*>(
+                                           src + ((((size_t)img * CB + cb) * Hs + y) * Ws + x) * 16) + q);
+                nz = v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f;
+            }
+        }
+        nz = __any_sync(0xffffffffu, nz);
+        if (lane == 0) zflag[f] = nz ? 1 : 0;
+    }
+}
+
 __global__ void tc_zero_kernel(int* flag, unsigned long long* cnt) {
     *flag = 0;
     *cnt = 0;
@@ -379,7 +451,8 @@ void choose_box(int Ho, int Wo, int* bw, int* bh) {
 template <int BN, int KB>
 cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUtensorMap& mbhi,
                       const CUtensorMap& mblo, const TcGeo& g, int N, float* dst, const int* nonfinite,
-                      const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st) {
+                      const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st,
+                      const uint8_t* zflag) {
     constexpr size_t STAGE = KB * (2 * TC_BM * 64 + 2 * BN * 64);
     // 4 stages (3 stages at BN = 128 with two CTAs per SM measured 1-3% slower);
     // 2-block stages: as many stages as fit 200 KB
@@ -404,7 +477,7 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     int ctas = persist_env > 0 ? persist_env : 148 * per_sm;
     if (ctas > gg.ntiles) ctas = gg.ntiles;
     dim3 grid((unsigned)ctas);
-    tc_conv_kernel<BN, ST, KB><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt, exec_ctr, epi);
+    tc_conv_kernel<BN, ST, KB><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt, exec_ctr, epi, zflag);
     note_launch();
     return cudaGetLastError();
 }
@@ -759,16 +832,35 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         cudaFreeAsync(scratch, st);
         return cudaErrorInvalidValue;
     }
+    // sparse mode: all-zero tile flags (SPC_TC_SKIP=0 disables the skip)
+    static const int skip_env = std::getenv("SPC_TC_SKIP") ? std::atoi(std::getenv("SPC_TC_SKIP")) : 1;
+    uint8_t* zflag = nullptr;
+    if (sparse && skip_env && (Cr / 16) / kb <= 64) {
+        const int NG = (Cr / 16) / kb;
+        const size_t nflags = (size_t)sh.N * NG * g.tiles_x * g.tiles_y;
+        e = cudaMallocAsync((void**)&zflag, nflags, st);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(scratch, st);
+            return e;
+        }
+        const int ylo = fwd ? -sh.padH : sh.padH - (sh.S - 1), yhi = fwd ? sh.S - 1 - sh.padH : sh.padH;
+        const int xlo = fwd ? -sh.padW : sh.padW - (sh.R - 1), xhi = fwd ? sh.R - 1 - sh.padW : sh.padW;
+        const size_t blocks = (nflags * 32 + 255) / 256;
+        tc_zero_tiles_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(
+            src, zflag, sh.N, Cr / 16, kb, Hs, Ws, g.tiles_x, g.tiles_y, g.bw, g.bh, ylo, yhi, xlo, xhi);
+        note_launch();
+    }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
     if (bn == 256)
-        e = launch_bn<256, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
+        e = launch_bn<256, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
     else if (bn == 128)
-        e = kb == 2 ? launch_bn<128, 2>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st)
-                    : launch_bn<128, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
+        e = kb == 2 ? launch_bn<128, 2>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag)
+                    : launch_bn<128, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
     else
-        e = launch_bn<64, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st);
+        e = launch_bn<64, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
     // non-finite source or filter: the FFMA tile kernel with the reference's exact skip semantics
     if (e == cudaSuccess) e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
+    if (zflag) cudaFreeAsync(zflag, st);
     cudaFreeAsync(scratch, st);
     return e;
 }

@@ -186,3 +186,29 @@ def test_tc_bww_nonfinite_takes_exact_path(sp):
     fin = np.isfinite(f32)
     assert np.array_equal(tc[fin], f32[fin])
     assert ctc == c32
+
+
+@pytest.mark.parametrize("comp", [0, 1])
+@pytest.mark.parametrize("shape", [(2, 128, 256, 28, 28, 3, 3), (3, 64, 64, 40, 40, 3, 3), (2, 256, 128, 14, 14, 1, 1)])
+def test_tc_skips_all_zero_tiles_exactly(sp, shape, comp):
+    """Spatially structured zeros (whole channel blocks, half images): the
+    variant's all-zero tile skip (north_star: "skips all-zero tiles") leaves
+    outputs and exact counters unchanged, and sparse == dense bit for bit."""
+    rng = np.random.default_rng(17 + comp)
+    N, C, K, H, W, R, S = shape
+    sh = sp.ConvShape.make(N, C, K, H, W, R, S, 1, 1)
+    t = sh.astuple()
+    chans = C if comp == 0 else K
+    hh, ww = (H, W) if comp == 0 else (sh.out_h(), sh.out_w())
+    a = _gauss_relu(rng, (N, chans, hh, ww), 0.5)
+    a[:, 16:48] = 0.0                  # two whole 16-channel blocks
+    a[0, :, : hh // 2] = 0.0           # top half of image 0
+    a[-1, :, :, ww // 3:] = 0.0        # right two thirds of the last image
+    g = (rng.standard_normal((K, C, S, R)) * np.sqrt(2.0 / (C * R * S))).astype(np.float32)
+    ref = O.dense(comp, t, a, g)
+    _, res, got = _run(sp, sh, comp, a, g)
+    assert O.max_abs_rel(got, ref) <= TC_TOL
+    want = O.expected_counts(t, O.plan(t, comp, V, 30, 0), a)
+    assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+    _, _, dgot = _run(sp, sh, comp, a, g, mode=1)
+    assert np.array_equal(dgot, got)
