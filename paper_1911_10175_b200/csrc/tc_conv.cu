@@ -906,7 +906,9 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     g.ctiles = (sh.C + cw - 1) / cw;
     g.stages = (long)NB * sh.Hp * sh.Wp;
     const long tiles = (long)g.tgroups * g.ktiles * g.ctiles;
-    long splits = (148 + tiles - 1) / tiles;  // about one wave of CTAs
+    // at most one wave of CTAs (one per SM): rounding up would leave a second
+    // wave of a few CTAs as long as the first (VGG conv3_2: 162 CTAs -> 144)
+    long splits = 148 / tiles > 0 ? 148 / tiles : 1;
     const long min_stages = 64;               // keep each split's pipeline long
     if (splits > g.stages / min_stages) splits = g.stages / min_stages > 0 ? g.stages / min_stages : 1;
     g.splits = (int)splits;
