@@ -145,11 +145,14 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 // A [N][CB][H][W][16] fp32 tensor (ActNCHWc) as a 5-D map with box
 // {16, b1 (x), b2 (y), b3 (channel blocks), 1}, SWIZZLE_64B, OOB -> 0.
-inline bool make_act_map(CUtensorMap* m, const float* p, int N, int CB, int H, int W, int b1, int b2, int b3) {
+// `str` = traversal stride over x and y (the box then spans str * b1 x str * b2
+// source pixels and lands b1 x b2 of them).
+inline bool make_act_map(CUtensorMap* m, const float* p, int N, int CB, int H, int W, int b1, int b2, int b3,
+                         int str = 1) {
     cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)CB, (cuuint64_t)N};
     cuuint64_t strides[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)CB * H * W * 64};
-    cuuint32_t box[5] = {16, (cuuint32_t)b1, (cuuint32_t)b2, (cuuint32_t)b3, 1};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    cuuint32_t box[5] = {16, (cuuint32_t)(b1 * str), (cuuint32_t)(b2 * str), (cuuint32_t)b3, 1};
+    cuuint32_t es[5] = {1, (cuuint32_t)str, (cuuint32_t)str, 1, 1};
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(p), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

@@ -39,6 +39,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -60,18 +61,31 @@ constexpr int TC_THREADS = 320;
 // TMEM allocations are powers of two >= 32 columns
 constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 
-// Geometry of one launch, by value.
+// Geometry of one FWD/BWI launch, by value.  The output is covered by up to
+// four parity classes (four only for BWI with stride 2, whose output pixel
+// (2m + cy, 2n + cx) takes the taps v with (cy + pad - v) even from dY pixel
+// m + (cy + pad - v) / 2 -- the reference's inverse row map, kernel_impl.hpp:
+// 85-89); each class is a stride-1 (or, FWD stride 2, strided-source) conv
+// over its own grid, listed as a tap table.
+struct TcClass {
+    int oy, ox;              // first output row / column; position = (oy + os*m, ox + os*n)
+    int Hc, Wc;              // class grid extent
+    int tiles_x, tiles_y;    // 128-pixel boxes over the class grid
+    int tile0;               // first tile of the class within one (N tile, image)
+    int ntap;
+    int tap[9], dy[9], dx[9];  // filter tap v*R+u; source = (sstr*m + dy, sstr*n + dx)
+};
 struct TcGeo {
     int Ho, Wo;        // output spatial extent
     int bw, bh;        // output box (bw * bh = 128)
-    int tiles_x, tiles_y;
+    int os, sstr;      // output position stride of the class grids; source traversal stride
+    int ncls;
+    TcClass cls[4];
+    int tiles_img;     // tiles per (N tile, image)
     int Co;            // output channels
     int RB;            // reduction blocks (input channels / 16)
-    int R, S;          // filter columns, rows
-    int sgn;           // +1 FWD (src = out + tap - pad), -1 BWI (src = out + pad - tap)
-    int padW, padH;
     int seg;           // pipeline stages per TMEM accumulation segment
-    int N, ntiles;     // images; tiles = N * tiles_x * tiles_y * (Co / BN)
+    int N, ntiles;     // images; tiles = N * tiles_img * (Co / BN)
     size_t out_img;    // floats per output image
 };
 
@@ -96,18 +110,16 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent: this CTA runs tiles blockIdx.x, + gridDim.x, ...; tile t =
-    // (n tile, image, box row, box column), n tile slowest so the CTAs in
-    // flight share one filter slice in L2
-    const int txy = g.tiles_x * g.tiles_y;
+    // (n tile, image, class, box row, box column), n tile slowest so the CTAs
+    // in flight share one filter slice in L2
+    const int txy = g.tiles_img;
     const int ntiles = g.ntiles;
     const int NG = g.RB / KB;                 // channel-block groups (one per tap sweep)
-    const int taps = g.R * g.S;
     const int D = g.seg;                      // stages per accumulation segment
     // all-zero tile skipping (sparse mode): zflag[img][group][tile] = 0 when the
-    // tile's source box (all taps) is zero in the group's channels; every role
-    // reads the same flags, so the skipped stages never enter the pipeline
-    // a tile's flags as a bit mask (NG <= 64, host-checked), loaded once per
-    // tile by each role: no flag load on the MMA issue path
+    // tile's source box (all taps) is zero in the group's channels; a tile's
+    // flags are loaded once per tile as a bit mask (NG <= 64, host-checked) by
+    // every role, so skipped stages never enter the pipeline
     auto live_mask = [&](int img, int tt) {
         if (zflag == nullptr) return ~0ull;
         unsigned long long m = 0;
@@ -119,9 +131,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
     // order), so skipping leaves every segment's summation grouping -- and the
     // result -- bitwise equal to dense mode; a segment with no live stage is
     // skipped by the MMA issuer and the epilogue alike.
-    const int nstage = NG * taps;
-    const int nseg = (nstage + D - 1) / D;
-    auto seg_live = [&](unsigned long long lm, int ls) {
+    auto seg_live = [&](unsigned long long lm, int ls, int taps, int nstage) {
         const int g0 = (ls * D) / taps, g1 = (min(ls * D + D, nstage) - 1) / taps;
         const unsigned long long span = (g1 - g0 == 63) ? ~0ull : ((2ull << (g1 - g0)) - 1) << g0;
         return (lm & span) != 0;
@@ -132,14 +142,17 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
     auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
     auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * ST + b); };
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * ST + 2 + b); };
-    auto tile_coords = [&](int t, int& img, int& x0, int& y0, int& n0, int& tt) {
+    auto tile_coords = [&](int t, int& img, int& x0, int& y0, int& n0, int& tt, int& c) {
         const int nt = t / (g.N * txy);
         int r = t - nt * g.N * txy;
         img = r / txy;
         r -= img * txy;
         tt = r;
-        const int ty = r / g.tiles_x;
-        x0 = (r - ty * g.tiles_x) * g.bw;
+        c = 0;
+        while (c + 1 < g.ncls && r >= g.cls[c + 1].tile0) ++c;
+        r -= g.cls[c].tile0;
+        const int ty = r / g.cls[c].tiles_x;
+        x0 = (r - ty * g.cls[c].tiles_x) * g.bw;
         y0 = ty * g.bh;
         n0 = nt * BN;
     };
@@ -176,25 +189,25 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
             int gi = 0;  // stage counter across this CTA's tiles (the smem ring continues)
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int img, x0, y0, n0, tt;
-                tile_coords(t, img, x0, y0, n0, tt);
+                int img, x0, y0, n0, tt, c;
+                tile_coords(t, img, x0, y0, n0, tt, c);
+                const TcClass& C = g.cls[c];
                 const unsigned long long lm = live_mask(img, tt);
                 for (int grp = 0; grp < NG; ++grp) {
                     if (!((lm >> grp) & 1ull)) continue;
                     const int rb = grp * KB;
-                    for (int v = 0; v < g.S; ++v)
-                        for (int u = 0; u < g.R; ++u, ++gi) {
-                            const int s = gi % ST;
-                            if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
-                            const uint32_t st = sbase + s * STAGE;
-                            mbar_expect_tx(full_bar(s), STAGE);
-                            const int sx = x0 + g.sgn * (u - g.padW), sy = y0 + g.sgn * (v - g.padH);
-                            tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
-                            tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
-                            const int brow = (v * g.R + u) * g.RB + rb;
-                            tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
-                            tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
-                        }
+                    for (int j = 0; j < C.ntap; ++j, ++gi) {
+                        const int s = gi % ST;
+                        if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
+                        const uint32_t st = sbase + s * STAGE;
+                        mbar_expect_tx(full_bar(s), STAGE);
+                        const int sx = g.sstr * x0 + C.dx[j], sy = g.sstr * y0 + C.dy[j];
+                        tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
+                        tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
+                        const int brow = C.tap[j] * g.RB + rb;
+                        tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
+                        tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
+                    }
                 }
             }
         }
@@ -203,12 +216,13 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
             const uint32_t idesc = tf32_idesc<BN>();
             int gi = 0, gseg = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int img, x0, y0, n0, tt;
-                tile_coords(t, img, x0, y0, n0, tt);
+                int img, x0, y0, n0, tt, c;
+                tile_coords(t, img, x0, y0, n0, tt, c);
+                const int taps = g.cls[c].ntap, nstage = NG * taps, nseg = (nstage + D - 1) / D;
                 const unsigned long long lm = live_mask(img, tt);
                 int ne = 0;  // live segments of this tile
                 for (int ls = 0; ls < nseg; ++ls) {
-                    if (!seg_live(lm, ls)) continue;
+                    if (!seg_live(lm, ls, taps, nstage)) continue;
                     const int sg = gseg + ne++, buf = sg & 1;
                     if (sg >= 2) mbar_wait(tempty_bar(buf), ((sg >> 1) - 1) & 1);
                     const uint32_t tm = tmem + buf * BN;
@@ -255,15 +269,17 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
         const size_t plane = (size_t)g.Ho * g.Wo * 16;
         int gseg = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            int img, x0, y0, n0, tt;
-            tile_coords(t, img, x0, y0, n0, tt);
+            int img, x0, y0, n0, tt, c;
+            tile_coords(t, img, x0, y0, n0, tt, c);
+            const TcClass& C = g.cls[c];
+            const int taps = C.ntap, nstage = NG * taps, nseg = (nstage + D - 1) / D;
             float acc[HALF];
 #pragma unroll
             for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
             const unsigned long long lm = live_mask(img, tt);
             int ne = 0;  // an all-zero tile has none: outputs = epi(0)
             for (int ls = 0; ls < nseg; ++ls) {
-                if (!seg_live(lm, ls)) continue;
+                if (!seg_live(lm, ls, taps, nstage)) continue;
                 const int sg = gseg + ne++, buf = sg & 1;
                 mbar_wait_sleep(tfull_bar(buf), (sg >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -279,8 +295,8 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
                 if (lane == 0) mbar_arrive(tempty_bar(buf));
             }
             gseg += ne;
-            const int y = y0 + py, x = x0 + px;
-            if (y < g.Ho && x < g.Wo) {
+            if (y0 + py < C.Hc && x0 + px < C.Wc) {
+                const int y = C.oy + g.os * (y0 + py), x = C.ox + g.os * (x0 + px);
                 float* out = dst + (size_t)img * g.out_img + ((size_t)y * g.Wo + x) * 16;
 #pragma unroll
                 for (int j = 0; j < HALF / 16; ++j) {
@@ -316,7 +332,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
 __global__ void tc_split_src_kernel(const float* __restrict__ src, float* __restrict__ lo, size_t n4, int Hs,
                                     int Ws, int Ho, int Wo, int R, int S, int padW, int padH, int bwi,
                                     unsigned scale, unsigned long long* __restrict__ cnt,
-                                    int* __restrict__ nonfinite) {
+                                    int* __restrict__ nonfinite, int str = 1) {
     unsigned long long acc = 0;
     int bad = 0;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n4; e += (size_t)gridDim.x * blockDim.x) {
@@ -336,13 +352,25 @@ __global__ void tc_split_src_kernel(const float* __restrict__ src, float* __rest
             const int xx = (int)(pix % Ws);
             const int yy = (int)((pix / Ws) % Hs);
             int rows = 0, cols = 0;
+            // FWD: output rows y' with y'*str + v - pad = y (oracle.cpp:160-190);
+            // BWI: input rows y = y'*str + v - pad inside the image (:195-230)
             for (int v = 0; v < S; ++v) {
-                const int o = bwi ? yy + v - padH : yy + padH - v;  // stride 1
-                rows += (o >= 0 && o < Ho) ? 1 : 0;
+                if (bwi) {
+                    const int o = yy * str + v - padH;
+                    rows += (o >= 0 && o < Ho) ? 1 : 0;
+                } else {
+                    const int n = yy + padH - v;
+                    rows += (n >= 0 && n % str == 0 && n / str < Ho) ? 1 : 0;
+                }
             }
             for (int u = 0; u < R; ++u) {
-                const int o = bwi ? xx + u - padW : xx + padW - u;
-                cols += (o >= 0 && o < Wo) ? 1 : 0;
+                if (bwi) {
+                    const int o = xx * str + u - padW;
+                    cols += (o >= 0 && o < Wo) ? 1 : 0;
+                } else {
+                    const int n = xx + padW - u;
+                    cols += (n >= 0 && n % str == 0 && n / str < Wo) ? 1 : 0;
+                }
             }
             acc += (unsigned long long)nz * rows * cols * scale;
         }
@@ -380,12 +408,12 @@ __global__ void tc_split_filter_kernel(const float* __restrict__ f, float* __res
 }
 
 // zflag[img][group][tile] = 1 when the tile's source box -- the output box
-// widened by every tap's offset ([ylo, yhi] x [xlo, xhi]), clipped to the
+// (x sstr) widened by every tap's offset ([ylo, yhi] x [xlo, xhi]), clipped to the
 // image -- holds a nonzero in the group's KB 16-channel blocks, else 0 (all
 // the tile's MMAs for that group would multiply zeros).  One warp per flag.
 __global__ void tc_zero_tiles_kernel(const float* __restrict__ src, uint8_t* __restrict__ zflag, int N, int CB,
                                      int KB, int Hs, int Ws, int tiles_x, int tiles_y, int bw, int bh, int ylo,
-                                     int yhi, int xlo, int xhi) {
+                                     int yhi, int xlo, int xhi, int sstr) {
     const int NG = CB / KB, txy = tiles_x * tiles_y;
     const long nflags = (long)N * NG * txy;
     const int lane = threadIdx.x & 31;
@@ -395,8 +423,8 @@ __global__ void tc_zero_tiles_kernel(const float* __restrict__ src, uint8_t* __r
         const int grp = (int)((f / txy) % NG);
         const int img = (int)(f / ((long)txy * NG));
         const int ty = tt / tiles_x, tx = tt - ty * tiles_x;
-        const int ya = max(ty * bh + ylo, 0), yb = min(ty * bh + bh - 1 + yhi, Hs - 1);
-        const int xa = max(tx * bw + xlo, 0), xb = min(tx * bw + bw - 1 + xhi, Ws - 1);
+        const int ya = max(sstr * ty * bh + ylo, 0), yb = min(sstr * (ty * bh + bh - 1) + yhi, Hs - 1);
+        const int xa = max(sstr * tx * bw + xlo, 0), xb = min(sstr * (tx * bw + bw - 1) + xhi, Ws - 1);
         const int nx = xb - xa + 1, ny = yb - ya + 1;
         bool nz = false;
         if (nx > 0 && ny > 0) {
@@ -468,7 +496,7 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     }
     TcGeo gg = g;
     gg.N = N;
-    gg.ntiles = N * g.tiles_x * g.tiles_y * (g.Co / BN);
+    gg.ntiles = N * g.tiles_img * (g.Co / BN);
     // persistent CTAs: as many as fit per SM (2 for BN <= 128: their
     // prologues / stores overlap each other's main loops), or fewer tiles
     // (measured, VGG conv1_2 FWD at BN = 64: 1 CTA/SM 75, 2 CTAs/SM 117 TFLOP/s)
@@ -503,6 +531,7 @@ struct TcBwwGeo {
     int ktiles, ctiles, splits;
     int cw, tpc, tgroups;  // channels per tap in a c tile, taps stacked along N (BN = tpc * cw), tap groups
     long stages;     // ceil(N / 16) * Hp * Wp
+    int str;         // stride (source pixel = str * output pixel + tap - pad)
     int seg;
 };
 
@@ -586,7 +615,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const int tap = tg * g.tpc + j;
                     const int v = tap / g.R, u = tap - v * g.R;
                     // a missing tap of the last group loads an all-out-of-bounds box (zeros)
-                    const int sx = tap < g.R * g.S ? xp + u - g.padW : -(1 << 20), sy = yp + v - g.padH;
+                    const int sx = tap < g.R * g.S ? g.str * xp + u - g.padW : -(1 << 20);
+                    const int sy = g.str * yp + v - g.padH;
                     const uint32_t boff = (uint32_t)(j * g.cw * 64);
                     tma_load_5d(st + 2 * A_BYTES + boff, &map_bhi, full_bar(s), 0, ct * g.cw, sx, sy, ib);
                     tma_load_5d(st + 2 * A_BYTES + B_BYTES + boff, &map_blo, full_bar(s), 0, ct * g.cw, sx, sy, ib);
@@ -763,7 +793,7 @@ cudaError_t launch_bww_bn(const CUtensorMap& ahi, const CUtensorMap& alo, const 
 bool tc_conv_supported(bool fwd, const DevShape& sh, int V) {
     (void)fwd;
     if (V != 16) return false;
-    if (sh.O != 1 || sh.P != 1) return false;
+    if (sh.O != sh.P || (sh.O != 1 && sh.O != 2)) return false;
     if (!((sh.R == 3 && sh.S == 3) || (sh.R == 1 && sh.S == 1))) return false;
     if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
     const int Co = fwd ? sh.K : sh.C;
@@ -794,23 +824,65 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         filt, bhi, blo, Co, Cr, sh.R, sh.S, nonfinite);
     tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(src, lo, nsrc / 4, Hs, Ws, Ho, Wo, sh.R, sh.S, sh.padW, sh.padH,
                                                  fwd ? 0 : 1, (unsigned)(Co / 16), (sparse && exec_ctr) ? cnt : nullptr,
-                                                 nonfinite);
+                                                 nonfinite, sh.O);
     note_launch(3);
 
+    // Output classes and tap tables (TcGeo): FWD (any stride) and BWI stride 1
+    // are one class over the whole output; BWI stride 2 splits the output into
+    // its 4 parity classes (P/include/spconv/tensor.hpp:57-66 restated per class).
+    const int str = sh.O;  // O == P (tc_conv_supported)
     TcGeo g;
+    std::memset(&g, 0, sizeof(g));
     g.Ho = Ho;
     g.Wo = Wo;
-    choose_box(Ho, Wo, &g.bw, &g.bh);
-    g.tiles_x = (Wo + g.bw - 1) / g.bw;
-    g.tiles_y = (Ho + g.bh - 1) / g.bh;
     g.Co = Co;
     g.RB = Cr / 16;
-    g.R = sh.R;
-    g.S = sh.S;
-    g.sgn = fwd ? 1 : -1;
-    g.padW = sh.padW;
-    g.padH = sh.padH;
     g.out_img = (size_t)Co * Ho * Wo;
+    g.sstr = fwd ? str : 1;
+    g.os = (!fwd && str == 2) ? 2 : 1;
+    g.ncls = (!fwd && str == 2) ? 4 : 1;
+    int ylo = 1 << 20, yhi = -(1 << 20), xlo = 1 << 20, xhi = -(1 << 20);  // tap offset extents (flags)
+    {
+        // one box shape for every class (the classes of BWI stride 2 differ by at most one row / column)
+        const int Hc0 = (Ho + g.os - 1) / g.os, Wc0 = (Wo + g.os - 1) / g.os;
+        choose_box(Hc0, Wc0, &g.bw, &g.bh);
+        int tile0 = 0;
+        for (int c = 0; c < g.ncls; ++c) {
+            TcClass& C = g.cls[c];
+            const int cy = g.ncls == 4 ? c >> 1 : 0, cx = g.ncls == 4 ? c & 1 : 0;
+            C.oy = cy;
+            C.ox = cx;
+            C.Hc = (Ho - cy + g.os - 1) / g.os;
+            C.Wc = (Wo - cx + g.os - 1) / g.os;
+            C.tiles_x = (C.Wc + g.bw - 1) / g.bw;
+            C.tiles_y = (C.Hc + g.bh - 1) / g.bh;
+            C.tile0 = tile0;
+            tile0 += C.tiles_x * C.tiles_y;
+            C.ntap = 0;
+            for (int v = 0; v < sh.S; ++v)
+                for (int u = 0; u < sh.R; ++u) {
+                    int dy, dx;
+                    if (fwd) {  // source = str * out + tap - pad (kernel_impl.hpp:82-84)
+                        dy = v - sh.padH;
+                        dx = u - sh.padW;
+                    } else {    // out = str * y' + tap - pad  =>  y' = (out + pad - tap) / str
+                        const int ny = cy + sh.padH - v, nx = cx + sh.padW - u;
+                        if (((ny % str) + str) % str || ((nx % str) + str) % str) continue;
+                        dy = ny / str;
+                        dx = nx / str;
+                    }
+                    C.tap[C.ntap] = v * sh.R + u;
+                    C.dy[C.ntap] = dy;
+                    C.dx[C.ntap] = dx;
+                    ++C.ntap;
+                    ylo = std::min(ylo, dy);
+                    yhi = std::max(yhi, dy);
+                    xlo = std::min(xlo, dx);
+                    xhi = std::max(xhi, dx);
+                }
+        }
+        g.tiles_img = tile0;
+    }
     // SPC_TC_SEG overrides the segment length (accuracy / speed experiments)
     static const int seg_env = std::getenv("SPC_TC_SEG") ? std::atoi(std::getenv("SPC_TC_SEG")) : 0;
     g.seg = seg_env > 0 ? seg_env : 8;  // error 1.2-1.4e-6 measured
@@ -825,8 +897,8 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     // 117 -> 103), BN = 256 one (a 96 KB stage would leave 2 stages).
     static const int kb_env = std::getenv("SPC_TC_KB") ? std::atoi(std::getenv("SPC_TC_KB")) : 0;
     const int kb = (kb_env == 1 || bn != 128 || (Cr / 16) % 2) ? 1 : 2;
-    if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb) ||
-        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb) ||
+    if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb, g.sstr) ||
+        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb, g.sstr) ||
         !make_filter_map(&mbhi, bhi, taps * (Cr / 16), Co, bn, kb) ||
         !make_filter_map(&mblo, blo, taps * (Cr / 16), Co, bn, kb)) {
         cudaFreeAsync(scratch, st);
@@ -835,19 +907,18 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     // sparse mode: all-zero tile flags (SPC_TC_SKIP=0 disables the skip)
     static const int skip_env = std::getenv("SPC_TC_SKIP") ? std::atoi(std::getenv("SPC_TC_SKIP")) : 1;
     uint8_t* zflag = nullptr;
-    if (sparse && skip_env && (Cr / 16) / kb <= 64) {
+    if (sparse && skip_env && (Cr / 16) / kb <= 64 && g.ncls == 1) {
         const int NG = (Cr / 16) / kb;
-        const size_t nflags = (size_t)sh.N * NG * g.tiles_x * g.tiles_y;
+        const size_t nflags = (size_t)sh.N * NG * g.tiles_img;
         e = cudaMallocAsync((void**)&zflag, nflags, st);
         if (e != cudaSuccess) {
             cudaFreeAsync(scratch, st);
             return e;
         }
-        const int ylo = fwd ? -sh.padH : sh.padH - (sh.S - 1), yhi = fwd ? sh.S - 1 - sh.padH : sh.padH;
-        const int xlo = fwd ? -sh.padW : sh.padW - (sh.R - 1), xhi = fwd ? sh.R - 1 - sh.padW : sh.padW;
         const size_t blocks = (nflags * 32 + 255) / 256;
         tc_zero_tiles_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(
-            src, zflag, sh.N, Cr / 16, kb, Hs, Ws, g.tiles_x, g.tiles_y, g.bw, g.bh, ylo, yhi, xlo, xhi);
+            src, zflag, sh.N, Cr / 16, kb, Hs, Ws, g.cls[0].tiles_x, g.cls[0].tiles_y, g.bw, g.bh, ylo, yhi, xlo,
+            xhi, g.sstr);
         note_launch();
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
@@ -867,7 +938,7 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
 
 bool tc_bww_supported(const DevShape& sh, int V) {
     if (V != 16) return false;
-    if (sh.O != 1 || sh.P != 1) return false;
+    if (sh.O != sh.P || (sh.O != 1 && sh.O != 2)) return false;
     if (!((sh.R == 3 && sh.S == 3) || (sh.R == 1 && sh.S == 1))) return false;
     if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
     if (sh.C % 16 || sh.K % 16) return false;
@@ -905,6 +976,7 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     g.ktiles = (sh.K + TC_BM - 1) / TC_BM;
     g.ctiles = (sh.C + cw - 1) / cw;
     g.stages = (long)NB * sh.Hp * sh.Wp;
+    g.str = sh.O;
     const long tiles = (long)g.tgroups * g.ktiles * g.ctiles;
     // at most one wave of CTAs (one per SM): rounding up would leave a second
     // wave of a few CTAs as long as the first (VGG conv3_2: 162 CTAs -> 144)
@@ -936,13 +1008,15 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     if (check_input) {
         if (cp)
             tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(chk, nullptr, nD / 4, sh.H, sh.W, sh.Hp, sh.Wp, sh.R, sh.S,
-                                                         sh.padW, sh.padH, 0, (unsigned)(sh.K / 16), cp, nonfinite);
+                                                         sh.padW, sh.padH, 0, (unsigned)(sh.K / 16), cp, nonfinite,
+                                                         sh.O);
         tc_to_hwcn_split_kernel<true><<<tb_d, 256, 0, st>>>(chk, d_hi, d_lo, sh.N, sh.C, HW, nonfinite);
         tc_to_hwcn_split_kernel<false><<<tb_y, 256, 0, st>>>(oth, y_hi, y_lo, sh.N, sh.K, HWp, nonfinite);
     } else {
         if (cp)
             tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(chk, nullptr, nY / 4, sh.Hp, sh.Wp, sh.H, sh.W, sh.R, sh.S,
-                                                         sh.padW, sh.padH, 1, (unsigned)(sh.C / 16), cp, nonfinite);
+                                                         sh.padW, sh.padH, 1, (unsigned)(sh.C / 16), cp, nonfinite,
+                                                         sh.O);
         tc_to_hwcn_split_kernel<true><<<tb_y, 256, 0, st>>>(chk, y_hi, y_lo, sh.N, sh.K, HWp, nonfinite);
         tc_to_hwcn_split_kernel<false><<<tb_d, 256, 0, st>>>(oth, d_hi, d_lo, sh.N, sh.C, HW, nonfinite);
     }

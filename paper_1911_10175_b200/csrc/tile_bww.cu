@@ -567,6 +567,24 @@ cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& 
     const bool kk4 = (check_input ? sh.K : sh.C) % 128 == 0;
 #define SPC_B(CI, KK, CB, NWC, TH, TW, R) \
     return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, 1>(sparse, sh, chk, oth, dst, exec_ctr, st, sel, want)
+#define SPC_B2(CI, KK, CB, NWC, TH, TW, R) \
+    return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, 2>(sparse, sh, chk, oth, dst, exec_ctr, st, sel, want)
+    if (sh.O == 2) {  // the stride-2 configurations of launch_tile_bww
+        if (check_input) {
+            if (sh.R == 3) {
+                if (kk4) SPC_B2(true, 4, 2, 4, 2, 4, 3);
+                SPC_B2(true, 2, 4, 4, 2, 4, 3);
+            }
+            if (kk4) SPC_B2(true, 4, 4, 4, 4, 8, 1);
+            SPC_B2(true, 2, 4, 4, 4, 8, 1);
+        }
+        if (sh.R == 3) {
+            if (kk4) SPC_B2(false, 4, 2, 4, 2, 2, 3);
+            SPC_B2(false, 2, 2, 4, 2, 4, 3);
+        }
+        if (kk4) SPC_B2(false, 4, 4, 4, 4, 8, 1);
+        SPC_B2(false, 2, 4, 4, 4, 8, 1);
+    }
     if (check_input) {
         if (sh.R == 3) {
             if (kk4) SPC_B(true, 4, 1, 8, 7, 4, 3);
@@ -579,6 +597,7 @@ cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& 
     if (kk4) SPC_B(false, 4, 4, 4, 4, 8, 1);
     SPC_B(false, 2, 4, 4, 4, 8, 1);
 #undef SPC_B
+#undef SPC_B2
 }
 
 }  // namespace spc

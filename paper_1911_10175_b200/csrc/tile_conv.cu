@@ -778,6 +778,28 @@ cudaError_t launch_tile_conv_when(bool fwd, bool sparse, const DevShape& sh, con
                                   float* dst, unsigned long long* exec_ctr, cudaStream_t st, const Epi& epi,
                                   const int* sel, int want) {
     const bool kk4 = (fwd ? sh.K : sh.C) % 128 == 0;
+    if (sh.O == 2) {  // the stride-2 tile configurations of launch_tile_conv
+        if (sh.R == 3) {
+            if (fwd)
+                return kk4 ? launch_cfg<true, 4, 4, 4, 2, 1, 3, 3, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr,
+                                                                                 st, sel, want, epi, Gate{})
+                           : launch_cfg<true, 2, 4, 4, 2, 1, 3, 3, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr,
+                                                                                 st, sel, want, epi, Gate{});
+            return kk4 ? launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                              sel, want, epi, Gate{})
+                       : launch_cfg<false, 2, 4, 8, 2, 1, 3, 3, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                              sel, want, epi, Gate{});
+        }
+        if (fwd)
+            return kk4 ? launch_cfg<true, 4, 4, 8, 2, 1, 1, 1, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                             sel, want, epi, Gate{})
+                       : launch_cfg<true, 2, 4, 8, 2, 1, 1, 1, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,
+                                                                             sel, want, epi, Gate{});
+        return kk4 ? launch_cfg<false, 4, 4, 8, 2, 1, 1, 1, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, sel,
+                                                                          want, epi, Gate{})
+                   : launch_cfg<false, 2, 4, 8, 2, 1, 1, 1, 2, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st, sel,
+                                                                          want, epi, Gate{});
+    }
     if (sh.R == 3) {
         if (kk4)
             return fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(sparse, sh, src, filt, dst, exec_ctr, st,

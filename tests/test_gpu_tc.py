@@ -212,3 +212,56 @@ def test_tc_skips_all_zero_tiles_exactly(sp, shape, comp):
     assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
     _, _, dgot = _run(sp, sh, comp, a, g, mode=1)
     assert np.array_equal(dgot, got)
+
+
+S2_SHAPES = [
+    (2, 64, 128, 56, 56, 3, 3),     # ResNet stage-transition 3x3 s2
+    (3, 128, 128, 15, 13, 3, 3),    # odd extents: ragged parity classes
+    (2, 256, 512, 28, 28, 1, 1),    # 1x1 s2 projection
+    (2, 64, 256, 13, 11, 1, 1),
+]
+
+
+@pytest.mark.parametrize("shape", S2_SHAPES)
+@pytest.mark.parametrize("comp", [0, 1])
+def test_tc_stride2_matches_oracle(sp, shape, comp):
+    """Stride 2 on the tensor cores: FWD with TMA traversal stride 2, BWI as
+    its 4 output parity classes (gap columns exactly 0 for 1x1)."""
+    rng = np.random.default_rng((hash(shape) + 7 * comp) & 0xFFFF)
+    N, C, K, H, W, R, S = shape
+    sh = sp.ConvShape.make(N, C, K, H, W, R, S, 2, 2)
+    t = sh.astuple()
+    a = _gauss_relu(rng, (N, C, H, W) if comp == 0 else (N, K, sh.out_h(), sh.out_w()), 0.6)
+    g = (rng.standard_normal((K, C, S, R)) * np.sqrt(2.0 / (C * R * S))).astype(np.float32)
+    ref = O.dense(comp, t, a, g)
+    _, res, got = _run(sp, sh, comp, a, g)
+    assert O.max_abs_rel(got, ref) <= TC_TOL, (shape, comp, O.max_abs_rel(got, ref))
+    if comp == 1 and R == 1:
+        assert not got[:, :, 1::2, :].any() and not got[:, :, :, 1::2].any()  # stride gaps exactly 0
+    want = O.expected_counts(t, O.plan(t, comp, V, 30, 0), a)
+    assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+    _, _, dgot = _run(sp, sh, comp, a, g, mode=1)
+    assert np.array_equal(dgot, got)
+
+
+@pytest.mark.parametrize("shape", [(16, 64, 128, 56, 56, 3, 3), (20, 128, 256, 14, 14, 1, 1)])
+@pytest.mark.parametrize("check", [0, 1])
+def test_tc_bww_stride2_matches_oracle(sp, shape, check):
+    rng = np.random.default_rng((hash(shape) + check) & 0xFFFF)
+    N, C, K, H, W, R, S = shape
+    sh = sp.ConvShape.make(N, C, K, H, W, R, S, 2, 2)
+    t = sh.astuple()
+    d = _gauss_relu(rng, (N, C, H, W), 0.6)
+    dy = _gauss_relu(rng, (N, K, sh.out_h(), sh.out_w()), 0.5)
+    ref = O.dense(2, t, d, dy)
+    if check == 0:
+        ba, bb = sp.pack_act_chwnn(d, V), sp.pack_act_nchwc(dy, V)
+    else:
+        ba, bb = sp.pack_act_nchwc(d, V), sp.pack_act_chwnn(dy, V)
+    pl = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck(check))
+    with sp.math_mode(sp.Math.tf32x3):
+        res = sp.run_parallel(ba.to("cuda"), bb.to("cuda"), sh, pl, sp.RunMode.sparse)
+    got = sp.unpack(res.out).cpu().numpy()
+    assert O.max_abs_rel(got, ref) <= TC_TOL, (shape, check, O.max_abs_rel(got, ref))
+    want = O.expected_counts(t, O.plan(t, 2, V, 30, check), d if check == 0 else dy)
+    assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
