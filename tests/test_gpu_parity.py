@@ -432,10 +432,12 @@ def test_host_path_pipelined_chunks_match_device_path(sp):
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 @pytest.mark.parametrize("cfg,idx", [("resnet50_b64", 1), ("resnet50_b64", 2), ("resnet50_b64", 11),
                                      ("resnet34_b64", 7), ("resnet34_b64", 8), ("vgg16_b32", 8)])
-def test_baseline_layers_match_reference_cpu(sp, cfg, idx):
+@pytest.mark.parametrize("math", ["fp32", "tf32x3"])
+def test_baseline_layers_match_reference_cpu(sp, cfg, idx, math):
     """BASELINE layer geometries (stride-2 3x3, 1x1 reduce/expand/projection,
     VGG 512-channel) at full spatial size and a 4-image batch: GPU vs the
-    reference's own CPU kernels on identical inputs, all three passes."""
+    reference's own CPU kernels on identical inputs, all three passes, in both
+    arithmetics (FP32 FFMA; the 3xTF32 tensor-core variant, same 1e-5 bar)."""
     import torch
     from paper_1911_10175_b200 import workloads as wl
     V = 16
@@ -461,8 +463,9 @@ def test_baseline_layers_match_reference_cpu(sp, cfg, idx):
             lb = sp.Layout.act_nchwc if check == 0 else sp.Layout.act_chwnn
             ba = sp.BlockedTensor(la, V, sh.N, sh.C, sh.H, sh.W, data=ta)
             bb = sp.BlockedTensor(lb, V, sh.N, sh.K, sh.out_h(), sh.out_w(), data=tb)
-        _, res, got = run(sp, sh, comp, check, V, ba, bb, 0)
-        assert O.max_abs_rel(got, ref_out) <= TOL, (cfg, idx, comp, check)
+        with sp.math_mode(sp.Math[math]):
+            _, res, got = run(sp, sh, comp, check, V, ba, bb, 0)
+        assert O.max_abs_rel(got, ref_out) <= TOL, (cfg, idx, comp, check, math)
         assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
         assert res.counters.checked_vectors == ref_cnt["checked_vectors"]
         r.close()
