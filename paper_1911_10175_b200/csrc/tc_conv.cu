@@ -57,7 +57,8 @@ using namespace tc;
 
 constexpr int TC_BM = 128;
 constexpr int TC_ST = 4;          // pipeline stages
-constexpr int TC_THREADS = 320;
+constexpr int TC_THREADS = 320;       // BWW: TMA, MMA, 8 drain / epilogue warps
+constexpr int TC_CONV_THREADS = 384;  // FWD/BWI: + 2 warps that split A into hi / lo in shared memory
 // TMEM allocations are powers of two >= 32 columns
 constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 
@@ -89,13 +90,18 @@ struct TcGeo {
     size_t out_img;    // floats per output image
 };
 
-template <int BN, int ST, int KB>
-__global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two CTAs per SM (<= 96 registers)
+// INK: A's lo half computed in shared memory by two converter warps (1x1
+// convs: each A element is used by one stage, and the split pass's lo copy --
+// a full write + read of the source -- would dominate a 1x1 layer's traffic);
+// otherwise (3x3: A elements recur in up to 9 tap stages) A_lo is a TMA load
+// of the lo copy the split pass writes.
+template <int BN, int ST, int KB, bool INK>
+__global__ void __launch_bounds__(TC_CONV_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two CTAs per SM (<= 80 registers)
     tc_conv_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
-                   const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-                   TcGeo g, float* __restrict__ dst, const int* __restrict__ nonfinite,
-                   const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr,
-                   Epi epi, const uint8_t* __restrict__ zflag) {
+                   const __grid_constant__ CUtensorMap map_bhi,
+                   const __grid_constant__ CUtensorMap map_blo, TcGeo g, float* __restrict__ dst,
+                   const int* __restrict__ nonfinite, const unsigned long long* __restrict__ cnt_tmp,
+                   unsigned long long* __restrict__ exec_ctr, Epi epi, const uint8_t* __restrict__ zflag) {
     if (__ldg(nonfinite) != 0) return;  // the exact FFMA kernel runs instead
     // a stage = KB 16-channel blocks of one tap: A = KB sub-tiles of 128 rows x
     // 64 B (hi, then lo), B = KB sub-tiles of BN rows x 64 B (hi, then lo)
@@ -105,8 +111,9 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
     constexpr int HALF = BN / 2;  // accumulator columns per epilogue thread
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);  // full[ST] empty[ST] tfull[2] tempty[2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
+    // full[ST] empty[ST] tfull[2] tempty[2] conv[ST]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent: this CTA runs tiles blockIdx.x, + gridDim.x, ...; tile t =
@@ -142,6 +149,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
     auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
     auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * ST + b); };
     auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * ST + 2 + b); };
+    auto conv_bar = [&](int s) { return bar0 + 8u * (2 * ST + 4 + s); };
     auto tile_coords = [&](int t, int& img, int& x0, int& y0, int& n0, int& tt, int& c) {
         const int nt = t / (g.N * txy);
         int r = t - nt * g.N * txy;
@@ -161,6 +169,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
         for (int s = 0; s < ST; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
+            mbar_init(conv_bar(s), 2);  // one arrival per converter warp (INK)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull_bar(b), 1);
@@ -181,10 +190,45 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp >= 10) {
+        // Converters (INK only; otherwise idle until the final barrier): A_lo = A_hi - tf32_trunc(A_hi), elementwise on the
+        // swizzled tile (same positions, so the layout carries over), for every
+        // live stage in pipeline order; then the MMA may read the stage.  No lo
+        // copy of the source tensor exists in HBM.
+        const int ct = threadIdx.x - 10 * 32;  // 0 .. 63
+        int gi = 0;
+        for (int t = INK ? (int)blockIdx.x : ntiles; t < ntiles; t += gridDim.x) {
+            int img, x0, y0, n0, tt, c;
+            tile_coords(t, img, x0, y0, n0, tt, c);
+            const unsigned long long lm = live_mask(img, tt);
+            const int taps = g.cls[c].ntap;
+            for (int grp = 0; grp < NG; ++grp) {
+                if (!((lm >> grp) & 1ull)) continue;
+                for (int j = 0; j < taps; ++j, ++gi) {
+                    const int s = gi % ST;
+                    mbar_wait(full_bar(s), (gi / ST) & 1);
+                    const float4* hi = reinterpret_cast<const float4*>(smem + s * STAGE);
+                    float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + A_BYTES);
+#pragma unroll
+                    for (int q = ct; q < (int)(A_BYTES / 16); q += 64) {
+                        const float4 x = hi[q];
+                        float4 l;
+                        l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+                        l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+                        l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+                        l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+                        lo[q] = l;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(conv_bar(s));
+                }
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+            if (!INK) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
             int gi = 0;  // stage counter across this CTA's tiles (the smem ring continues)
@@ -200,10 +244,10 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
                         const int s = gi % ST;
                         if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
                         const uint32_t st = sbase + s * STAGE;
-                        mbar_expect_tx(full_bar(s), STAGE);
+                        mbar_expect_tx(full_bar(s), INK ? STAGE - A_BYTES : STAGE);  // INK: A_lo computed in smem
                         const int sx = g.sstr * x0 + C.dx[j], sy = g.sstr * y0 + C.dy[j];
                         tma_load_5d(st, &map_hi, full_bar(s), 0, sx, sy, rb, img);
-                        tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
+                        if (!INK) tma_load_5d(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, rb, img);
                         const int brow = C.tap[j] * g.RB + rb;
                         tma_load_3d(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, n0, brow);
                         tma_load_3d(st + 2 * A_BYTES + B_BYTES, &map_blo, full_bar(s), 0, n0, brow);
@@ -231,6 +275,7 @@ __global__ void __launch_bounds__(TC_THREADS, BN == 64 ? 2 : 1)  // BN = 64: two
                         if (!((lm >> (it / taps)) & 1ull)) continue;
                         const int s = gi % ST;
                         mbar_wait(full_bar(s), (gi / ST) & 1);
+                        if (INK) mbar_wait(conv_bar(s), (gi / ST) & 1);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         const uint32_t st = sbase + s * STAGE;
 #pragma unroll
@@ -476,9 +521,8 @@ void choose_box(int Ho, int Wo, int* bw, int* bh) {
     }
 }
 
-template <int BN, int KB>
-cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUtensorMap& mbhi,
-                      const CUtensorMap& mblo, const TcGeo& g, int N, float* dst, const int* nonfinite,
+template <int BN, int KB, bool INK>
+cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUtensorMap& mbhi, const CUtensorMap& mblo, const TcGeo& g, int N, float* dst, const int* nonfinite,
                       const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st,
                       const uint8_t* zflag) {
     constexpr size_t STAGE = KB * (2 * TC_BM * 64 + 2 * BN * 64);
@@ -488,9 +532,9 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     const size_t smem = ST * STAGE + 1024 + 256;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB, INK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB, INK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -505,7 +549,8 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     int ctas = persist_env > 0 ? persist_env : 148 * per_sm;
     if (ctas > gg.ntiles) ctas = gg.ntiles;
     dim3 grid((unsigned)ctas);
-    tc_conv_kernel<BN, ST, KB><<<grid, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt, exec_ctr, epi, zflag);
+    tc_conv_kernel<BN, ST, KB, INK><<<grid, TC_CONV_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt,
+                                                                          exec_ctr, epi, zflag);
     note_launch();
     return cudaGetLastError();
 }
@@ -809,16 +854,17 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     const int taps = sh.R * sh.S;
     const size_t nsrc = (size_t)sh.N * Cr * Hs * Ws;
     const size_t nfilt = (size_t)Co * Cr * taps;
-    // scratch: [flag, pad][counter][src lo][filter hi][filter lo]
-    const size_t bytes = 256 + nsrc * 4 + 2 * nfilt * 4;
+    // scratch: [flag, pad][counter][filter hi][filter lo][src lo (3x3 only: 1x1 splits A in shared memory)]
+    const bool ink = sh.R == 1 && sh.S == 1;
+    const size_t bytes = 256 + 2 * nfilt * 4 + (ink ? 0 : nsrc * 4);
     uint8_t* scratch = nullptr;
     cudaError_t e = cudaMallocAsync((void**)&scratch, bytes, st);
     if (e != cudaSuccess) return e;
     int* nonfinite = reinterpret_cast<int*>(scratch);
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(scratch + 128);
-    float* lo = reinterpret_cast<float*>(scratch + 256);
-    float* bhi = lo + nsrc;
+    float* bhi = reinterpret_cast<float*>(scratch + 256);
     float* blo = bhi + nfilt;
+    float* lo = ink ? nullptr : blo + nfilt;
     tc_zero_kernel<<<1, 1, 0, st>>>(nonfinite, cnt);
     tc_split_filter_kernel<<<(unsigned)((nfilt + 255) / 256 < 148 * 8 ? (nfilt + 255) / 256 : 148 * 8), 256, 0, st>>>(
         filt, bhi, blo, Co, Cr, sh.R, sh.S, nonfinite);
@@ -898,7 +944,7 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     static const int kb_env = std::getenv("SPC_TC_KB") ? std::atoi(std::getenv("SPC_TC_KB")) : 0;
     const int kb = (kb_env == 1 || bn != 128 || (Cr / 16) % 2) ? 1 : 2;
     if (!make_act_map(&mhi, src, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb, g.sstr) ||
-        !make_act_map(&mlo, lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb, g.sstr) ||
+        !make_act_map(&mlo, ink ? src : lo, sh.N, Cr / 16, Hs, Ws, g.bw, g.bh, kb, g.sstr) ||
         !make_filter_map(&mbhi, bhi, taps * (Cr / 16), Co, bn, kb) ||
         !make_filter_map(&mblo, blo, taps * (Cr / 16), Co, bn, kb)) {
         cudaFreeAsync(scratch, st);
@@ -922,13 +968,16 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         note_launch();
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
+#define SPC_TCL(BN_, KB_)                                                                                      \
+    (ink ? launch_bn<BN_, KB_, true>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag)    \
+         : launch_bn<BN_, KB_, false>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag))
     if (bn == 256)
-        e = launch_bn<256, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
+        e = SPC_TCL(256, 1);
     else if (bn == 128)
-        e = kb == 2 ? launch_bn<128, 2>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag)
-                    : launch_bn<128, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
+        e = kb == 2 ? SPC_TCL(128, 2) : SPC_TCL(128, 1);
     else
-        e = launch_bn<64, 1>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
+        e = SPC_TCL(64, 1);
+#undef SPC_TCL
     // non-finite source or filter: the FFMA tile kernel with the reference's exact skip semantics
     if (e == cudaSuccess) e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
     if (zflag) cudaFreeAsync(zflag, st);
