@@ -159,7 +159,7 @@ spc_status spc_epilogue_apply(const spc_epilogue* epi, float* data, size_t n, vo
  * per-product rounding.  SPC_MATH_TF32X3: tcgen05 tensor cores with 3xTF32
  * split products (hi*hi + hi*lo + lo*hi, fp32 accumulate), its own stated
  * tolerance; used for the geometries it covers (V = 16,
- * stride 1, 3x3 pad 1 / 1x1 pad 0), the FP32 kernels elsewhere and for
+ * stride 1 or 2, 3x3 pad 1 / 1x1 pad 0), the FP32 kernels elsewhere and for
  * inputs holding Inf/NaN.  Per host thread; returns the previous mode, or -1
  * for an unknown mode (unchanged). */
 typedef enum { SPC_MATH_FP32 = 0, SPC_MATH_TF32X3 = 1 } spc_math;

@@ -21,21 +21,25 @@
 // kernel then exits at entry and the FFMA tile kernel (gated on the same flag)
 // computes the pass with the reference's exact skip semantics.
 //
-// GEMM view (one CTA = one 128-pixel output box x BN output channels):
-//   M = 128 output pixels: a BW x BH box of one image, BW*BH = 128
+// GEMM view (one tile = one 128-pixel output box x BN output channels; CTAs
+// are persistent and walk tiles n-tile-slowest):
+//   M = 128 output pixels: a BW x BH box of one image (or of one output parity
+//       class for BWI stride 2), BW*BH = 128
 //   N = BN output channels (64 / 128 / 256)
-//   reduction = (16-channel block rb, tap (v,u)): per step the A tile is the
+//   reduction = (KB 16-channel blocks, tap): per stage the A tile is the
 //   source box shifted by the tap (TMA 5-D tiled load from ActNCHWc
-//   [N][C/16][H][W][16]: 64-byte rows, SWIZZLE_64B, out-of-image pixels
-//   zero-filled by TMA = the virtual padding), the B tile is the tap's
-//   [BN][16] filter slice from a K-major copy the prep kernel writes.
-// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
-// MMA issuer (one elected thread), warps 2-9 = accumulator drain + epilogue.
-// The MMAs accumulate a segment of `seg` pipeline stages into one of two TMEM
-// buffers (2 x BN columns) while the epilogue warps add the other buffer's
-// partial sums into fp32 registers; the last segment's drain is followed by
-// the store (TMEM -> registers -> ActNCHWc, fused Epi).  4-stage mbarrier
-// pipeline for the operands.
+//   [N][C/16][H][W][16]: 64-byte rows, SWIZZLE_64B, traversal stride 2 for FWD
+//   stride 2, out-of-image pixels zero-filled by TMA = the virtual padding),
+//   the B tile is the tap's [BN][16] filter slice from a K-major copy the prep
+//   kernel writes.
+// Warp roles (384 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// MMA issuer (one thread), warps 2-9 = accumulator drain + epilogue, warps
+// 10-11 = A hi/lo splitters (1x1 only).  The MMAs accumulate a segment of
+// `seg` pipeline stages into one of two TMEM buffers (2 x BN columns) while the
+// epilogue warps add the other buffer's partial sums into fp32 registers; the
+// last segment's drain is followed by the store (TMEM -> registers ->
+// ActNCHWc, fused Epi), which overlaps the next tile's MMAs.  All-zero tiles
+// (sparse mode) are skipped.  BWW (tc_bww_kernel, below) has its own notes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
