@@ -776,45 +776,57 @@ __global__ void tc_bww_reduce_kernel(const float* __restrict__ partial, float* _
 // channel) and 1 KB contiguous writes (16 ch x 16 images of one pixel).
 // Flags non-finite values.
 template <bool FROM_CHWNN>
-__global__ void tc_to_hwcn_split_kernel(const float* __restrict__ in, float* __restrict__ hi,
-                                        float* __restrict__ lo, int N, int C, int HW,
-                                        int* __restrict__ nonfinite) {
-    __shared__ float t[16 * 16 * 17];
+__global__ void __launch_bounds__(256) tc_to_hwcn_split_kernel(const float* __restrict__ in, float* __restrict__ hi,
+                                                               float* __restrict__ lo, int N, int C, int HW,
+                                                               int* __restrict__ nonfinite) {
+    __shared__ float t[16 * 16 * 17];  // [pixel][channel][image], rows padded to 17
     const int pblocks = (HW + 15) / 16;
     const int pb = blockIdx.x % pblocks;
     const int cb = (blockIdx.x / pblocks) % (C / 16);
     const int ib = blockIdx.x / (pblocks * (C / 16));
     const int tid = threadIdx.x;
     const int p0 = pb * 16;
-    const int px = tid >> 4, l = tid & 15;
     int bad = 0;
-#pragma unroll 4
-    for (int j = 0; j < 16; ++j) {
-        float x = 0.0f;
+    // reads: 1024 float4 = 16 runs of 1 KB (one per channel, or per image)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int q = tid + 256 * k;
+        const int j = q >> 6, px = (q & 63) >> 2, l4 = (q & 3) * 4;
+        float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         if (p0 + px < HW) {
-            if (FROM_CHWNN) {  // j = channel, l = image lane
-                x = __ldg(in + (((size_t)ib * C + cb * 16 + j) * HW + p0 + px) * 16 + l);
-                t[(px * 16 + j) * 17 + l] = x;
-            } else {           // j = image lane, l = channel
-                const int img = ib * 16 + j;
-                if (img < N) x = __ldg(in + (((size_t)img * (C / 16) + cb) * HW + p0 + px) * 16 + l);
-                t[(px * 16 + l) * 17 + j] = x;
+            if (FROM_CHWNN) {  // j = channel, l4 = first of 4 image lanes
+                x = __ldg(reinterpret_cast<const float4*>(in + (((size_t)ib * C + cb * 16 + j) * HW + p0 + px) * 16 + l4));
+            } else if (ib * 16 + j < N) {  // j = image lane, l4 = first of 4 channels
+                x = __ldg(reinterpret_cast<const float4*>(
+                    in + (((size_t)(ib * 16 + j) * (C / 16) + cb) * HW + p0 + px) * 16 + l4));
             }
-        } else {
-            t[(px * 16 + (FROM_CHWNN ? j : l)) * 17 + (FROM_CHWNN ? l : j)] = 0.0f;
         }
-        bad |= !isfinite(x);
+        bad |= !isfinite(x.x) | !isfinite(x.y) | !isfinite(x.z) | !isfinite(x.w);
+        const float v[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (FROM_CHWNN) t[(px * 16 + j) * 17 + l4 + e] = v[e];
+            else t[(px * 16 + l4 + e) * 17 + j] = v[e];
+        }
     }
     __syncthreads();
-    // write pixel p0 + p: channels cb*16 .. +15 x 16 images (1 KB contiguous)
-#pragma unroll 4
-    for (int r = 0; r < 16; ++r) {
-        const int p = r, c = tid >> 4, i = tid & 15;
-        if (p0 + p >= HW) break;
-        const float x = t[(p * 16 + c) * 17 + i];
-        const size_t o = (((size_t)ib * HW + p0 + p) * C + cb * 16 + c) * 16 + i;
-        hi[o] = x;
-        lo[o] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    // writes: pixel p0 + p = channels cb*16 .. +15 x 16 images (1 KB contiguous), float4 stores
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int q = tid + 256 * k;
+        const int p = q >> 6, c = (q & 63) >> 2, i4 = (q & 3) * 4;
+        if (p0 + p < HW) {
+            const float* r = t + (p * 16 + c) * 17 + i4;
+            const float4 x = make_float4(r[0], r[1], r[2], r[3]);
+            float4 l;
+            l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+            l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+            l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+            l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+            const size_t o = (((size_t)ib * HW + p0 + p) * C + cb * 16 + c) * 16 + i4;
+            *reinterpret_cast<float4*>(hi + o) = x;
+            *reinterpret_cast<float4*>(lo + o) = l;
+        }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(nonfinite, 1);
 }
