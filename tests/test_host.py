@@ -226,3 +226,22 @@ def test_no_device_fails_loudly(sp):
         sp.sparse_fwd(a, b, sh, sp.plan(sh, sp.Component.fwd, 8))
     assert e.value.status == sp._lib.SPC_ERR_NO_DEVICE
     assert not sp.native_backend_available(16)
+
+
+def test_math_mode_is_per_thread_and_validated(sp):
+    """spc_set_math / spc_get_math (include/spconv_b200.h): FP32 by default,
+    unknown modes rejected with the mode unchanged, per host thread."""
+    import threading
+    L = sp._lib.load()
+    assert sp.get_math() == sp.Math.fp32
+    assert L.spc_set_math(7) == -1 and sp.get_math() == sp.Math.fp32
+    with sp.math_mode(sp.Math.tf32x3):
+        assert sp.get_math() == sp.Math.tf32x3
+        seen = []
+        th = threading.Thread(target=lambda: seen.append(sp.get_math()))
+        th.start()
+        th.join()
+        assert seen == [sp.Math.fp32]  # another host thread keeps its own mode
+    assert sp.get_math() == sp.Math.fp32
+    with pytest.raises(sp.SpconvError):
+        sp.set_math(5)
