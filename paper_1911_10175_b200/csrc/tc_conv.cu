@@ -584,21 +584,25 @@ struct TcBwwGeo {
     int seg;
 };
 
-template <int BN>
+// PX = output pixels per stage (2 for small N tiles: 1x1, one tap, stride 1 --
+// twice the MMAs per barrier round trip, the small-N MMAs being issue-bound;
+// the 2 pixels are consecutive along x, one TMA box of {16, channels, 2}).
+template <int BN, int PX>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_bww_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                   const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                   TcBwwGeo g, float* __restrict__ partial, const int* __restrict__ nonfinite,
                   const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr) {
     if (__ldg(nonfinite) != 0) return;
-    constexpr uint32_t A_BYTES = TC_BM * 64;  // 8 k-blocks x 16 px x 64 B
-    constexpr uint32_t B_BYTES = BN * 64;     // BN/16 c-blocks x 16 px x 64 B
+    constexpr uint32_t A_BYTES = PX * TC_BM * 64;  // PX pixels x 128 k-rows x 64 B (16 images)
+    constexpr uint32_t B_BYTES = PX * BN * 64;     // PX pixels x BN c-rows x 64 B
     constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
+    constexpr int ST = PX == 1 ? TC_ST : (int)((200 * 1024) / STAGE);
     constexpr int HALF = BN / 2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_ST * STAGE);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_ST + 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // blockIdx.x = ((tap * ktiles + kt) * ctiles + ct), blockIdx.y = split
@@ -615,12 +619,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = smem_u32(bars);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (TC_ST + s); };
-    auto tfull_bar = [&](int bb) { return bar0 + 8u * (2 * TC_ST + bb); };
-    auto tempty_bar = [&](int bb) { return bar0 + 8u * (2 * TC_ST + 2 + bb); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int bb) { return bar0 + 8u * (2 * ST + bb); };
+    auto tempty_bar = [&](int bb) { return bar0 + 8u * (2 * ST + 2 + bb); };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_ST; ++s) {
+        for (int s = 0; s < ST; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
@@ -650,12 +654,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
             long t = t0;
-            int ib = (int)(t / ((long)g.Hp * g.Wp));
-            int rem = (int)(t - (long)ib * g.Hp * g.Wp);
-            int yp = rem / g.Wp, xp = rem - yp * g.Wp;
+            const long per_ib = (long)g.Hp * ((g.Wp + PX - 1) / PX);
+            int ib = (int)(t / per_ib);
+            int rem = (int)(t - (long)ib * per_ib);
+            const int xw = (g.Wp + PX - 1) / PX;  // stages per output row
+            int yp = rem / xw, xp = (rem - yp * xw) * PX;
             for (int it = 0; it < niter; ++it) {
-                const int s = it % TC_ST;
-                if (it >= TC_ST) mbar_wait(empty_bar(s), ((it / TC_ST) - 1) & 1);
+                const int s = it % ST;
+                if (it >= ST) mbar_wait(empty_bar(s), ((it / ST) - 1) & 1);
                 const uint32_t st = sbase + s * STAGE;
                 mbar_expect_tx(full_bar(s), STAGE);
                 tma_load_5d(st, &map_ahi, full_bar(s), 0, kt * TC_BM, xp, yp, ib);
@@ -670,7 +676,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     tma_load_5d(st + 2 * A_BYTES + boff, &map_bhi, full_bar(s), 0, ct * g.cw, sx, sy, ib);
                     tma_load_5d(st + 2 * A_BYTES + B_BYTES + boff, &map_blo, full_bar(s), 0, ct * g.cw, sx, sy, ib);
                 }
-                if (++xp == g.Wp) {
+                if ((xp += PX) >= g.Wp) {
                     xp = 0;
                     if (++yp == g.Hp) {
                         yp = 0;
@@ -686,17 +692,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int seg = it / D, buf = seg & 1;
                 const bool first = it - seg * D == 0;
                 if (first && seg >= 2) mbar_wait(tempty_bar(buf), ((seg >> 1) - 1) & 1);
-                const int s = it % TC_ST;
-                mbar_wait(full_bar(s), (it / TC_ST) & 1);
+                const int s = it % ST;
+                mbar_wait(full_bar(s), (it / ST) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t st = sbase + s * STAGE;
                 const uint32_t tm = tmem + buf * BN;
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {  // images 0-7, 8-15 (32 bytes each)
-                    const uint64_t ahi = sw64_desc(st + 32 * k);
-                    const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
-                    const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
-                    const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + 32 * k);
+                for (int k = 0; k < 2 * PX; ++k) {  // per pixel: images 0-7, 8-15 (32 bytes each)
+                    const uint32_t ao = (k >> 1) * (TC_BM * 64) + 32 * (k & 1);
+                    const uint32_t bo = (k >> 1) * (BN * 64) + 32 * (k & 1);
+                    const uint64_t ahi = sw64_desc(st + ao);
+                    const uint64_t alo = sw64_desc(st + A_BYTES + ao);
+                    const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + bo);
+                    const uint64_t blo = sw64_desc(st + 2 * A_BYTES + B_BYTES + bo);
                     umma_tf32(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
                     umma_tf32(tm, ahi, blo, idesc, 1u);
                     umma_tf32(tm, ahi, bhi, idesc, 1u);
@@ -831,20 +839,22 @@ __global__ void __launch_bounds__(256) tc_to_hwcn_split_kernel(const float* __re
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(nonfinite, 1);
 }
 
-template <int BN>
+template <int BN, int PX>
 cudaError_t launch_bww_bn(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& bhi,
                           const CUtensorMap& blo, const TcBwwGeo& g, float* partial, const int* nonfinite,
                           const unsigned long long* cnt, unsigned long long* exec_ctr, cudaStream_t st) {
-    constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * BN * 64;
-    const size_t smem = TC_ST * STAGE + 1024 + 256;
+    constexpr size_t STAGE = (size_t)PX * (2 * TC_BM * 64 + 2 * BN * 64);
+    constexpr int ST = PX == 1 ? TC_ST : (int)((200 * 1024) / STAGE);
+    const size_t smem = ST * STAGE + 1024 + 256;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_bww_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(tc_bww_kernel<BN, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid((unsigned)(g.tgroups * g.ktiles * g.ctiles), (unsigned)g.splits);
-    tc_bww_kernel<BN><<<grid, TC_THREADS, smem, st>>>(ahi, alo, bhi, blo, g, partial, nonfinite, cnt, exec_ctr);
+    tc_bww_kernel<BN, PX><<<grid, TC_THREADS, smem, st>>>(ahi, alo, bhi, blo, g, partial, nonfinite, cnt, exec_ctr);
     note_launch();
     return cudaGetLastError();
 }
@@ -1040,8 +1050,10 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     g.C = sh.C;
     g.ktiles = (sh.K + TC_BM - 1) / TC_BM;
     g.ctiles = (sh.C + cw - 1) / cw;
-    g.stages = (long)NB * sh.Hp * sh.Wp;
     g.str = sh.O;
+    // two output pixels per stage for a small single-tap N tile (stride 1)
+    const int px = (tpc == 1 && BN <= 128 && sh.O == 1) ? 2 : 1;
+    g.stages = (long)NB * sh.Hp * ((sh.Wp + px - 1) / px);
     const long tiles = (long)g.tgroups * g.ktiles * g.ctiles;
     // at most one wave of CTAs (one per SM): rounding up would leave a second
     // wave of a few CTAs as long as the first (VGG conv3_2: 162 CTAs -> 144)
@@ -1089,7 +1101,7 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     CUtensorMap ahi, alo, bhi, blo;
     // pixel-major [NB][H][W][C][16] = 5-D (16, C, W, H, NB); boxes = one pixel's channel tile
     const int dY5[5] = {16, sh.K, sh.Wp, sh.Hp, NB}, dD5[5] = {16, sh.C, sh.W, sh.H, NB};
-    const int bA[5] = {16, TC_BM, 1, 1, 1}, bB[5] = {16, cw, 1, 1, 1};
+    const int bA[5] = {16, TC_BM, px, 1, 1}, bB[5] = {16, cw, px, 1, 1};
     if (!make_map5(&ahi, y_hi, dY5, bA) || !make_map5(&alo, y_lo, dY5, bA) || !make_map5(&bhi, d_hi, dD5, bB) ||
         !make_map5(&blo, d_lo, dD5, bB)) {
         cudaFreeAsync(scratch, st);
@@ -1097,13 +1109,15 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
     if (BN == 256)
-        e = launch_bww_bn<256>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+        e = launch_bww_bn<256, 1>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
     else if (BN == 192)
-        e = launch_bww_bn<192>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+        e = launch_bww_bn<192, 1>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
     else if (BN == 128)
-        e = launch_bww_bn<128>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+        e = px == 2 ? launch_bww_bn<128, 2>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st)
+                    : launch_bww_bn<128, 1>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
     else
-        e = launch_bww_bn<64>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
+        e = px == 2 ? launch_bww_bn<64, 2>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st)
+                    : launch_bww_bn<64, 1>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
     if (e == cudaSuccess) {
         tc_bww_reduce_kernel<<<148 * 4, 256, 0, st>>>(part, dst, g.splits, sh.K, sh.C, sh.R, sh.S, nonfinite);
         note_launch();
