@@ -265,3 +265,39 @@ def test_tc_bww_stride2_matches_oracle(sp, shape, check):
     assert O.max_abs_rel(got, ref) <= TC_TOL, (shape, check, O.max_abs_rel(got, ref))
     want = O.expected_counts(t, O.plan(t, 2, V, 30, check), d if check == 0 else dy)
     assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
+
+
+@pytest.mark.parametrize("R", [1, 3])
+@pytest.mark.parametrize("comp", [0, 1, 2])
+def test_tc_stride2_nonfinite_takes_exact_path(sp, R, comp):
+    """Inf/NaN with stride 2: the tensor-core kernels exit and the gated FFMA
+    stride-2 kernels produce the reference's exact skip semantics."""
+    rng = np.random.default_rng(31 + R + 5 * comp)
+    sh = sp.ConvShape.make(4, 64, 128, 12, 12, R, R, 2, 2)
+    hp, wp = sh.out_h(), sh.out_w()
+    d = _gauss_relu(rng, (4, 64, 12, 12), 0.5)
+    dy = _gauss_relu(rng, (4, 128, hp, wp), 0.5)
+    g = (rng.standard_normal((128, 64, R, R)) * 0.05).astype(np.float32)
+    if comp == 0:
+        d[1, 2, 4, 4] = np.nan
+        ba, bb = sp.pack_act_nchwc(d, V), sp.pack_filter(g, V)
+    elif comp == 1:
+        dy[2, 3, 1, 2] = np.inf
+        ba, bb = sp.pack_act_nchwc(dy, V), sp.pack_filter(g, V, True)
+    else:
+        dy[0, 5, 2, 2] = -np.inf
+        ba, bb = sp.pack_act_chwnn(d, V), sp.pack_act_nchwc(dy, V)
+    ba, bb = ba.to("cuda"), bb.to("cuda")
+    pl = sp.plan(sh, sp.Component(comp), V)
+    outs = []
+    for m in (sp.Math.fp32, sp.Math.tf32x3):
+        with sp.math_mode(m):
+            r = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse)
+            outs.append((sp.unpack(r.out).cpu().numpy(), r.counters.executed_vector_fmas))
+    (f32, c32), (tc, ctc) = outs
+    assert np.array_equal(np.isnan(tc), np.isnan(f32)) and np.array_equal(np.isinf(tc), np.isinf(f32))
+    fin = np.isfinite(f32)
+    # the fallback is an FFMA kernel (the tile kernel), the FP32 default for
+    # 1x1 BWW is the GEMM kernel: same products, possibly another summation order
+    assert O.max_abs_rel(tc[fin], f32[fin]) <= TC_TOL
+    assert ctc == c32
