@@ -559,6 +559,320 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- CTA pairs
+// tc_pair_kernel: the same FWD/BWI GEMM on a CTA pair (cluster of 2,
+// tcgen05.mma.cta_group::2, M = 256): each CTA of the pair loads its own
+// 128-pixel A tile and HALF of the BN filter rows, and the pair's leader issues
+// one M=256 MMA over both shared memories -- the filter bytes per SM halve, so
+// a stage is 32 KB instead of 48 and the ring is 6 stages deep.  Both CTAs'
+// TMA loads signal the leader's full barrier; the leader's MMA completion is
+// multicast to both CTAs' empty / TMEM-full barriers; both epilogues release a
+// TMEM buffer on the leader's barrier.  Tiles pair up within one N tile (the
+// filter half must match); one output class (FWD any stride, BWI stride 1).
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank0(uint32_t addr) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(addr));
+    return r;
+}
+__device__ __forceinline__ void tma_load_5d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(bar)
+        : "memory");
+}
+
+template <int BN, int ST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_pair_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                   const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo, TcGeo g,
+                   float* __restrict__ dst, const int* __restrict__ nonfinite,
+                   const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr, Epi epi,
+                   const uint8_t* __restrict__ zflag) {
+    if (__ldg(nonfinite) != 0) return;  // uniform over the pair (same flag)
+    constexpr uint32_t A_BYTES = TC_BM * 64;
+    constexpr uint32_t BH_BYTES = (BN / 2) * 64;  // this CTA's half of the filter rows
+    constexpr uint32_t STAGE = 2 * A_BYTES + 2 * BH_BYTES;
+    constexpr int HALF = BN / 2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);  // full[ST] empty[ST] tfull[2] tempty[2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
+    const uint32_t rank = cluster_rank();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int txy = g.tiles_img;
+    const int per_nt = g.N * txy;               // tiles per N tile
+    const int pairs_nt = (per_nt + 1) / 2;
+    const int npairs = pairs_nt * (g.Co / BN);
+    const int pair0 = blockIdx.x >> 1, pstep = gridDim.x >> 1;
+    const int NG = g.RB;
+    const int D = g.seg;
+    const TcClass& C = g.cls[0];
+    const int taps = C.ntap, nstage = NG * taps, nseg = (nstage + D - 1) / D;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * ST + b); };
+    auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * ST + 2 + b); };
+    // pair p -> (n tile, this CTA's tile); the partner of a last odd tile recomputes it (no store)
+    auto tile_of = [&](int p, uint32_t r, int& img, int& tt, int& x0, int& y0, int& n0, bool& own) {
+        const int nt = p / pairs_nt, pp = p - nt * pairs_nt;
+        int t = 2 * pp + (int)r;
+        own = t < per_nt;
+        if (!own) t = per_nt - 1;
+        img = t / txy;
+        tt = t - img * txy;
+        const int ty = tt / C.tiles_x;
+        x0 = (tt - ty * C.tiles_x) * g.bw;
+        y0 = ty * g.bh;
+        n0 = nt * BN;
+    };
+    auto mask_of = [&](int img, int tt) {
+        if (zflag == nullptr) return ~0ull;
+        unsigned long long m = 0;
+        for (int grp = 0; grp < NG; ++grp)
+            m |= (unsigned long long)(__ldg(zflag + ((size_t)img * NG + grp) * txy + tt) != 0) << grp;
+        return m;
+    };
+    // the pair's live mask: both tiles' flags (identical in both CTAs)
+    auto pair_mask = [&](int p) {
+        int img, tt, x0, y0, n0;
+        bool own;
+        tile_of(p, 0, img, tt, x0, y0, n0, own);
+        unsigned long long m = mask_of(img, tt);
+        tile_of(p, 1, img, tt, x0, y0, n0, own);
+        return m | mask_of(img, tt);
+    };
+    auto seg_live = [&](unsigned long long lm, int ls) {
+        const int g0 = (ls * D) / taps, g1 = (min(ls * D + D, nstage) - 1) / taps;
+        const unsigned long long span = (g1 - g0 == 63) ? ~0ull : ((2ull << (g1 - g0)) - 1) << g0;
+        return (lm & span) != 0;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), 16);  // 8 epilogue warps x 2 CTAs (leader's barrier)
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (blockIdx.x == 0 && cnt_tmp && exec_ctr) atomicAdd(exec_ctr, *cnt_tmp);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(tmem_cols(2 * BN))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+            int gi = 0;
+            for (int p = pair0; p < npairs; p += pstep) {
+                int img, tt, x0, y0, n0;
+                bool own;
+                tile_of(p, rank, img, tt, x0, y0, n0, own);
+                const unsigned long long lm = pair_mask(p);
+                for (int grp = 0; grp < NG; ++grp) {
+                    if (!((lm >> grp) & 1ull)) continue;
+                    for (int j = 0; j < taps; ++j, ++gi) {
+                        const int s = gi % ST;
+                        if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
+                        const uint32_t st = sbase + s * STAGE;
+                        // the leader expects both CTAs' bytes on its own barrier
+                        if (rank == 0) mbar_expect_tx(full_bar(s), 2 * STAGE);
+                        const int sx = g.sstr * x0 + C.dx[j], sy = g.sstr * y0 + C.dy[j];
+                        tma_load_5d_pair(st, &map_hi, full_bar(s), 0, sx, sy, grp, img);
+                        tma_load_5d_pair(st + A_BYTES, &map_lo, full_bar(s), 0, sx, sy, grp, img);
+                        const int brow = C.tap[j] * g.RB + grp;
+                        const int nb = n0 + (int)rank * (BN / 2);
+                        tma_load_3d_pair(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, nb, brow);
+                        tma_load_3d_pair(st + 2 * A_BYTES + BH_BYTES, &map_blo, full_bar(s), 0, nb, brow);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // instruction descriptor: M = 256 (the pair), N = BN, tf32, K-major
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                   ((uint32_t)(256 >> 4) << 24);
+            int gi = 0, gseg = 0;
+            for (int p = pair0; p < npairs; p += pstep) {
+                const unsigned long long lm = pair_mask(p);
+                int ne = 0;
+                for (int ls = 0; ls < nseg; ++ls) {
+                    if (!seg_live(lm, ls)) continue;
+                    const int sg = gseg + ne++, buf = sg & 1;
+                    if (sg >= 2) mbar_wait(tempty_bar(buf), ((sg >> 1) - 1) & 1);
+                    const uint32_t tm = tmem + buf * BN;
+                    bool first = true;
+                    for (int it = ls * D; it < min(ls * D + D, nstage); ++it) {
+                        if (!((lm >> (it / taps)) & 1ull)) continue;
+                        const int s = gi % ST;
+                        mbar_wait(full_bar(s), (gi / ST) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint32_t st = sbase + s * STAGE;
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const uint64_t ahi = sw64_desc(st + 32 * k);
+                            const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
+                            const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
+                            const uint64_t blo = sw64_desc(st + 2 * A_BYTES + BH_BYTES + 32 * k);
+                            umma_tf32_pair(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
+                            umma_tf32_pair(tm, ahi, blo, idesc, 1u);
+                            umma_tf32_pair(tm, ahi, bhi, idesc, 1u);
+                        }
+                        first = false;
+                        umma_commit_pair(empty_bar(s));
+                        ++gi;
+                    }
+                    umma_commit_pair(tfull_bar(buf));
+                }
+                gseg += ne;
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int m = q * 32 + lane;
+        const int py = m / g.bw, px = m - py * g.bw;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const size_t plane = (size_t)g.Ho * g.Wo * 16;
+        int gseg = 0;
+        for (int p = pair0; p < npairs; p += pstep) {
+            int img, tt, x0, y0, n0;
+            bool own;
+            tile_of(p, rank, img, tt, x0, y0, n0, own);
+            const unsigned long long lm = pair_mask(p);
+            float acc[HALF];
+#pragma unroll
+            for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
+            int ne = 0;
+            for (int ls = 0; ls < nseg; ++ls) {
+                if (!seg_live(lm, ls)) continue;
+                const int sg = gseg + ne++, buf = sg & 1;
+                mbar_wait_sleep(tfull_bar(buf), (sg >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    float v[16];
+                    tmem_ld16(tmem + lane_off + buf * BN + h * HALF + 16 * j, v);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) acc[16 * j + e] += v[e];
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                     map_to_rank0(tempty_bar(buf)))
+                                 : "memory");
+            }
+            gseg += ne;
+            if (own && y0 + py < C.Hc && x0 + px < C.Wc) {
+                const int y = y0 + py, x = x0 + px;
+                float* out = dst + (size_t)img * g.out_img + ((size_t)y * g.Wo + x) * 16;
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    const int kb = ((n0 + h * HALF) >> 4) + j;
+                    float* o = out + (size_t)kb * plane;
+                    float v[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = acc[16 * j + e];
+                    if (epi.active()) {
+                        const size_t base = (size_t)(o - dst);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = epi.apply(v[e], base + e);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; e += 4)
+                        *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // the partner no longer arrives on / reads this CTA's barriers and smem
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN))
+                     : "memory");
+    }
+}
+
+template <int BN>
+cudaError_t launch_pair(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUtensorMap& mbhi,
+                        const CUtensorMap& mblo, const TcGeo& g, int N, float* dst, const int* nonfinite,
+                        const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st,
+                        const uint8_t* zflag) {
+    constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * (BN / 2) * 64;
+    constexpr int ST = (int)((200 * 1024) / STAGE) > 8 ? 8 : (int)((200 * 1024) / STAGE);
+    const size_t smem = ST * STAGE + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tc_pair_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    TcGeo gg = g;
+    gg.N = N;
+    const long per_nt = (long)N * g.tiles_img;
+    const long npairs = ((per_nt + 1) / 2) * (g.Co / BN);
+    long ctas = 148;
+    if (ctas > 2 * npairs) ctas = 2 * npairs;
+    tc_pair_kernel<BN, ST><<<(unsigned)ctas, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, gg, dst, nonfinite, cnt,
+                                                                     exec_ctr, epi, zflag);
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ================================================================ BWW
 // dG[k, c, v, u] = sum_{i, y', x'} dY[i, k, y', x'] * D[i, c, y'+v-padH, x'+u-padW]
 // (P/src/kernel_impl.hpp:209-336, P/src/kernels.cpp:238-302), as one GEMM per
@@ -994,6 +1308,25 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         note_launch();
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
+    // CTA pairs (SPC_TC_PAIR=0 disables): 3x3 / 1x1 without the in-smem split,
+    // one output class, one block per stage
+    static const int pair_env = std::getenv("SPC_TC_PAIR") ? std::atoi(std::getenv("SPC_TC_PAIR")) : 1;
+    // (measured: +5-8% on the BN = 256 VGG layers, conv3_2 179 -> 190 TF/s; a BN = 128 pair with one block
+    // per stage lost to the single-CTA two-block stages, conv2_2 173 -> 132)
+    if (pair_env && !ink && g.ncls == 1 && kb == 1 && bn == 256) {
+        CUtensorMap mbhi2, mblo2;
+        if (!make_filter_map(&mbhi2, bhi, taps * (Cr / 16), Co, bn / 2, 1) ||
+            !make_filter_map(&mblo2, blo, taps * (Cr / 16), Co, bn / 2, 1)) {
+            cudaFreeAsync(scratch, st);
+            return cudaErrorInvalidValue;
+        }
+        e = launch_pair<256>(mhi, mlo, mbhi2, mblo2, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
+        if (e == cudaSuccess)
+            e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
+        if (zflag) cudaFreeAsync(zflag, st);
+        cudaFreeAsync(scratch, st);
+        return e;
+    }
 #define SPC_TCL(BN_, KB_)                                                                                      \
     (ink ? launch_bn<BN_, KB_, true>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag)    \
          : launch_bn<BN_, KB_, false>(mhi, mlo, mbhi, mblo, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag))
