@@ -1351,9 +1351,9 @@ bool tc_bww_supported(const DevShape& sh, int V) {
     if (sh.padW != (sh.R - 1) / 2 || sh.padH != (sh.S - 1) / 2) return false;
     if (sh.C % 16 || sh.K % 16) return false;
     if ((sh.K % 64) || (sh.C % 64)) return false;  // the exact fallback (tile BWW) needs 64-channel multiples
-    // M = 128 output-gradient channels per tile: with K = 64 half the MMA rows
-    // are padding and the FFMA tile BWW is faster (VGG conv1_2: 2.5 vs 3.4 ms)
-    if (sh.K < 128) return false;
+    // K = 64 wastes half of the M = 128 MMA rows but still beats the FFMA BWW
+    // since the one-wave split fix (VGG conv1_2 62 vs ~50 TF/s; ResNet-50 3x3
+    // 64-channel 55 vs 41)
     return tc::encode_fn() != nullptr;
 }
 
