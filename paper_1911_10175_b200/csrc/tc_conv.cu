@@ -381,11 +381,27 @@ __global__ void __launch_bounds__(TC_CONV_THREADS, BN == 64 ? 2 : 1)  // BN = 64
 __global__ void tc_split_src_kernel(const float* __restrict__ src, float* __restrict__ lo, size_t n4, int Hs,
                                     int Ws, int Ho, int Wo, int R, int S, int padW, int padH, int bwi,
                                     unsigned scale, unsigned long long* __restrict__ cnt,
-                                    int* __restrict__ nonfinite, int str = 1) {
+                                    int* __restrict__ nonfinite, int str = 1,
+                                    uint8_t* __restrict__ rowflag = nullptr) {
     unsigned long long acc = 0;
     int bad = 0;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n4; e += (size_t)gridDim.x * blockDim.x) {
         const float4 x = __ldg(reinterpret_cast<const float4*>(src) + e);
+        if (rowflag) {
+            // rowflag[(image, channel block, row)] = 1 once the row holds a nonzero
+            // (zero-tile skip); a warp's 32 float4 nearly always share one row:
+            // one store for the warp then, per-lane stores otherwise (benign races,
+            // flags only go 0 -> 1)
+            const size_t row = e / (4 * (size_t)Ws);
+            const bool nz = x.x != 0.0f || x.y != 0.0f || x.z != 0.0f || x.w != 0.0f;
+            const unsigned act = __activemask();
+            const size_t row0 = __shfl_sync(act, row, __ffs(act) - 1);
+            if (__all_sync(act, row == row0)) {
+                if (__any_sync(act, nz) && (int)(threadIdx.x & 31) == __ffs(act) - 1) rowflag[row0] = 1;
+            } else if (nz) {
+                rowflag[row] = 1;
+            }
+        }
         if (lo) {
             float4 l;
             l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -456,41 +472,24 @@ __global__ void tc_split_filter_kernel(const float* __restrict__ f, float* __res
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(nonfinite, 1);
 }
 
-// zflag[img][group][tile] = 1 when the tile's source box -- the output box
-// (x sstr) widened by every tap's offset ([ylo, yhi] x [xlo, xhi]), clipped to the
-// image -- holds a nonzero in the group's KB 16-channel blocks, else 0 (all
-// the tile's MMAs for that group would multiply zeros).  One warp per flag.
-__global__ void tc_zero_tiles_kernel(const float* __restrict__ src, uint8_t* __restrict__ zflag, int N, int CB,
-                                     int KB, int Hs, int Ws, int tiles_x, int tiles_y, int bw, int bh, int ylo,
-                                     int yhi, int xlo, int xhi, int sstr) {
+// zflag[img][group][tile] = 1 when any source row of the tile's box -- the
+// output rows (x sstr) widened by the taps' row offsets [ylo, yhi], clipped to
+// the image -- holds a nonzero in the group's KB channel blocks (rowflag from
+// the split pass; whole image rows, so the skip is row-granular).
+__global__ void tc_zero_tiles_kernel(const uint8_t* __restrict__ rowflag, uint8_t* __restrict__ zflag, int N, int CB,
+                                     int KB, int Hs, int tiles_x, int tiles_y, int bh, int ylo, int yhi, int sstr) {
     const int NG = CB / KB, txy = tiles_x * tiles_y;
     const long nflags = (long)N * NG * txy;
-    const int lane = threadIdx.x & 31;
-    for (long f = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5; f < nflags;
-         f += ((long)gridDim.x * blockDim.x) >> 5) {
+    for (long f = blockIdx.x * (long)blockDim.x + threadIdx.x; f < nflags; f += (long)gridDim.x * blockDim.x) {
         const int tt = (int)(f % txy);
         const int grp = (int)((f / txy) % NG);
         const int img = (int)(f / ((long)txy * NG));
-        const int ty = tt / tiles_x, tx = tt - ty * tiles_x;
+        const int ty = tt / tiles_x;
         const int ya = max(sstr * ty * bh + ylo, 0), yb = min(sstr * (ty * bh + bh - 1) + yhi, Hs - 1);
-        const int xa = max(sstr * tx * bw + xlo, 0), xb = min(sstr * (tx * bw + bw - 1) + xhi, Ws - 1);
-        const int nx = xb - xa + 1, ny = yb - ya + 1;
-        bool nz = false;
-        if (nx > 0 && ny > 0) {
-            const long per_cb = (long)ny * nx * 4;  // float4s per channel block
-            for (long e = lane; e < per_cb * KB && !nz; e += 32) {
-                const int cb = grp * KB + (int)(e / per_cb);
-                long r = e % per_cb;
-                const int y = ya + (int)(r / (nx * 4));
-                r %= nx * 4;
-                const int x = xa + (int)(r >> 2), q = (int)(r & 3);
-                const float4 v = __ldg(reinterpret_cast<const float4*>(
-                                           src + ((((size_t)img * CB + cb) * Hs + y) * Ws + x) * 16) + q);
-                nz = v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f;
-            }
-        }
-        nz = __any_sync(0xffffffffu, nz);
-        if (lane == 0) zflag[f] = nz ? 1 : 0;
+        uint8_t nz = 0;
+        for (int cb = grp * KB; cb < grp * KB + KB && !nz; ++cb)
+            for (int y = ya; y <= yb && !nz; ++y) nz = rowflag[((size_t)img * CB + cb) * Hs + y];
+        zflag[f] = nz;
     }
 }
 
@@ -1208,10 +1207,7 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     tc_zero_kernel<<<1, 1, 0, st>>>(nonfinite, cnt);
     tc_split_filter_kernel<<<(unsigned)((nfilt + 255) / 256 < 148 * 8 ? (nfilt + 255) / 256 : 148 * 8), 256, 0, st>>>(
         filt, bhi, blo, Co, Cr, sh.R, sh.S, nonfinite);
-    tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(src, lo, nsrc / 4, Hs, Ws, Ho, Wo, sh.R, sh.S, sh.padW, sh.padH,
-                                                 fwd ? 0 : 1, (unsigned)(Co / 16), (sparse && exec_ctr) ? cnt : nullptr,
-                                                 nonfinite, sh.O);
-    note_launch(3);
+    note_launch(2);
 
     // Output classes and tap tables (TcGeo): FWD (any stride) and BWI stride 1
     // are one class over the whole output; BWI stride 2 splits the output into
@@ -1227,7 +1223,7 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
     g.sstr = fwd ? str : 1;
     g.os = (!fwd && str == 2) ? 2 : 1;
     g.ncls = (!fwd && str == 2) ? 4 : 1;
-    int ylo = 1 << 20, yhi = -(1 << 20), xlo = 1 << 20, xhi = -(1 << 20);  // tap offset extents (flags)
+    int ylo = 1 << 20, yhi = -(1 << 20);  // tap row-offset extents (zero-tile flags)
     {
         // one box shape for every class (the classes of BWI stride 2 differ by at most one row / column)
         const int Hc0 = (Ho + g.os - 1) / g.os, Wc0 = (Wo + g.os - 1) / g.os;
@@ -1263,8 +1259,6 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
                     ++C.ntap;
                     ylo = std::min(ylo, dy);
                     yhi = std::max(yhi, dy);
-                    xlo = std::min(xlo, dx);
-                    xhi = std::max(xhi, dx);
                 }
         }
         g.tiles_img = tile0;
@@ -1290,21 +1284,31 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         cudaFreeAsync(scratch, st);
         return cudaErrorInvalidValue;
     }
-    // sparse mode: all-zero tile flags (SPC_TC_SKIP=0 disables the skip)
+    // sparse mode: all-zero tile flags from row flags the split pass marks
+    // (SPC_TC_SKIP=0 disables the skip)
     static const int skip_env = std::getenv("SPC_TC_SKIP") ? std::atoi(std::getenv("SPC_TC_SKIP")) : 1;
     uint8_t* zflag = nullptr;
-    if (sparse && skip_env && (Cr / 16) / kb <= 64 && g.ncls == 1) {
-        const int NG = (Cr / 16) / kb;
-        const size_t nflags = (size_t)sh.N * NG * g.tiles_img;
-        e = cudaMallocAsync((void**)&zflag, nflags, st);
+    uint8_t* rowflag = nullptr;
+    const bool skip = sparse && skip_env && (Cr / 16) / kb <= 64 && g.ncls == 1;
+    const size_t nrows = (size_t)sh.N * (Cr / 16) * Hs;
+    const size_t nflags = skip ? (size_t)sh.N * ((Cr / 16) / kb) * g.tiles_img : 0;
+    if (skip) {
+        e = cudaMallocAsync((void**)&rowflag, nrows + nflags, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(rowflag, 0, nrows, st);
         if (e != cudaSuccess) {
             cudaFreeAsync(scratch, st);
             return e;
         }
-        const size_t blocks = (nflags * 32 + 255) / 256;
-        tc_zero_tiles_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(
-            src, zflag, sh.N, Cr / 16, kb, Hs, Ws, g.cls[0].tiles_x, g.cls[0].tiles_y, g.bw, g.bh, ylo, yhi, xlo,
-            xhi, g.sstr);
+        zflag = rowflag + nrows;
+    }
+    tc_split_src_kernel<<<148 * 8, 256, 0, st>>>(src, lo, nsrc / 4, Hs, Ws, Ho, Wo, sh.R, sh.S, sh.padW, sh.padH,
+                                                 fwd ? 0 : 1, (unsigned)(Co / 16), (sparse && exec_ctr) ? cnt : nullptr,
+                                                 nonfinite, sh.O, rowflag);
+    note_launch();
+    if (skip) {
+        const size_t blocks = (nflags + 255) / 256;
+        tc_zero_tiles_kernel<<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, st>>>(
+            rowflag, zflag, sh.N, Cr / 16, kb, Hs, g.cls[0].tiles_x, g.cls[0].tiles_y, g.bh, ylo, yhi, g.sstr);
         note_launch();
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
@@ -1323,7 +1327,7 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         e = launch_pair<256>(mhi, mlo, mbhi2, mblo2, g, sh.N, dst, nonfinite, cnt, ex, epi, st, zflag);
         if (e == cudaSuccess)
             e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
-        if (zflag) cudaFreeAsync(zflag, st);
+        if (rowflag) cudaFreeAsync(rowflag, st);
         cudaFreeAsync(scratch, st);
         return e;
     }
@@ -1339,7 +1343,7 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
 #undef SPC_TCL
     // non-finite source or filter: the FFMA tile kernel with the reference's exact skip semantics
     if (e == cudaSuccess) e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
-    if (zflag) cudaFreeAsync(zflag, st);
+    if (rowflag) cudaFreeAsync(rowflag, st);
     cudaFreeAsync(scratch, st);
     return e;
 }
