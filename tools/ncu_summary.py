@@ -8,6 +8,7 @@ import sys
 
 
 def family(name):
+    name = name.replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
     n = re.sub(r"[<(].*", "", name).replace("void ", "").strip()
     m = re.search(r"<([^>]*)>\(", name)
     args = [a.strip().replace("(bool)", "").replace("(int)", "") for a in m.group(1).split(",")] if m else []

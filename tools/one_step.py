@@ -10,6 +10,9 @@ import paper_1911_10175_b200 as sp
 from paper_1911_10175_b200 import workloads as wl
 
 V = 16
+# `python tools/one_step.py tf32x3`: the same step with the 3xTF32 tensor-core variant
+if len(sys.argv) > 1:
+    sp.set_math(sp.Math[sys.argv[1]])
 gen = torch.Generator(device="cuda").manual_seed(1000)
 work = []
 for s in (0.4, 0.6, 0.8, 0.9):
