@@ -1072,6 +1072,177 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
+// tc_bww_pair_kernel: the BWW GEMM on a CTA pair (cluster of 2, M = 256 = two
+// k tiles): each CTA loads its own dY k tile and HALF of the 256 D channel rows
+// of the stage; the leader issues one cta_group::2 MMA (the FWD pair kernel's
+// protocol).  Single tap per CTA (tpc = 1), BN = 256, K a multiple of 256.
+// blockIdx.x = ((tap group * ctiles + ct) * ktiles + kt): a cluster = kt, kt+1.
+template <int ST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    tc_bww_pair_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                       const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                       TcBwwGeo g, float* __restrict__ partial, const int* __restrict__ nonfinite,
+                       const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr) {
+    if (__ldg(nonfinite) != 0) return;
+    constexpr int BN = 256;
+    constexpr uint32_t A_BYTES = TC_BM * 64;
+    constexpr uint32_t BH_BYTES = (BN / 2) * 64;
+    constexpr uint32_t STAGE = 2 * A_BYTES + 2 * BH_BYTES;
+    constexpr int HALF = BN / 2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
+    const uint32_t rank = cluster_rank();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int b = blockIdx.x;
+    const int kt = b % g.ktiles;
+    b /= g.ktiles;
+    const int ct = b % g.ctiles;
+    const int tap = b / g.ctiles;
+    const int v = tap / g.R, u = tap - v * g.R;
+    const int split = blockIdx.y;
+    const long t0 = g.stages * split / g.splits, t1 = g.stages * (split + 1) / g.splits;
+    const int niter = (int)(t1 - t0);
+    const int D = g.seg;
+    const int nseg = (niter + D - 1) / D;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = smem_u32(bars);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int bb) { return bar0 + 8u * (2 * ST + bb); };
+    auto tempty_bar = [&](int bb) { return bar0 + 8u * (2 * ST + 2 + bb); };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int bb = 0; bb < 2; ++bb) {
+            mbar_init(tfull_bar(bb), 1);
+            mbar_init(tempty_bar(bb), 16);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (blockIdx.x == 0 && blockIdx.y == 0 && cnt_tmp && exec_ctr) atomicAdd(exec_ctr, *cnt_tmp);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(tmem_cols(2 * BN))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0 && niter > 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+            long t = t0;
+            const long per_ib = (long)g.Hp * g.Wp;
+            int ib = (int)(t / per_ib);
+            int rem = (int)(t - (long)ib * per_ib);
+            int yp = rem / g.Wp, xp = rem - yp * g.Wp;
+            for (int it = 0; it < niter; ++it) {
+                const int s = it % ST;
+                if (it >= ST) mbar_wait(empty_bar(s), ((it / ST) - 1) & 1);
+                const uint32_t st = sbase + s * STAGE;
+                if (rank == 0) mbar_expect_tx(full_bar(s), 2 * STAGE);
+                tma_load_5d_pair(st, &map_ahi, full_bar(s), 0, kt * TC_BM, xp, yp, ib);
+                tma_load_5d_pair(st + A_BYTES, &map_alo, full_bar(s), 0, kt * TC_BM, xp, yp, ib);
+                const int sx = g.str * xp + u - g.padW, sy = g.str * yp + v - g.padH;
+                const int c0 = ct * BN + (int)rank * HALF;
+                tma_load_5d_pair(st + 2 * A_BYTES, &map_bhi, full_bar(s), 0, c0, sx, sy, ib);
+                tma_load_5d_pair(st + 2 * A_BYTES + BH_BYTES, &map_blo, full_bar(s), 0, c0, sx, sy, ib);
+                if (++xp == g.Wp) {
+                    xp = 0;
+                    if (++yp == g.Hp) {
+                        yp = 0;
+                        ++ib;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                   ((uint32_t)(256 >> 4) << 24);
+            for (int it = 0; it < niter; ++it) {
+                const int seg = it / D, buf = seg & 1;
+                const bool first = it - seg * D == 0;
+                if (first && seg >= 2) mbar_wait(tempty_bar(buf), ((seg >> 1) - 1) & 1);
+                const int s = it % ST;
+                mbar_wait(full_bar(s), (it / ST) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t st = sbase + s * STAGE;
+                const uint32_t tm = tmem + buf * BN;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint64_t ahi = sw64_desc(st + 32 * k);
+                    const uint64_t alo = sw64_desc(st + A_BYTES + 32 * k);
+                    const uint64_t bhi = sw64_desc(st + 2 * A_BYTES + 32 * k);
+                    const uint64_t blo = sw64_desc(st + 2 * A_BYTES + BH_BYTES + 32 * k);
+                    umma_tf32_pair(tm, alo, bhi, idesc, (first && k == 0) ? 0u : 1u);
+                    umma_tf32_pair(tm, ahi, blo, idesc, 1u);
+                    umma_tf32_pair(tm, ahi, bhi, idesc, 1u);
+                }
+                umma_commit_pair(empty_bar(s));
+                if (it - seg * D == D - 1 || it == niter - 1) umma_commit_pair(tfull_bar(buf));
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int krow = kt * TC_BM + q * 32 + lane;
+        float acc[HALF];
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        for (int seg = 0; seg < nseg; ++seg) {
+            const int buf = seg & 1;
+            mbar_wait_sleep(tfull_bar(buf), (seg >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < HALF / 16; ++j) {
+                float vv[16];
+                tmem_ld16(tmem + lane_off + buf * BN + h * HALF + 16 * j, vv);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) acc[16 * j + e] += vv[e];
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                 map_to_rank0(tempty_bar(buf)))
+                             : "memory");
+        }
+        if (krow < g.K) {
+#pragma unroll
+            for (int j = 0; j < HALF; j += 4) {
+                const int c = ct * BN + h * HALF + j;
+                if (c < g.C) {
+                    float* o = partial + (((size_t)split * g.R * g.S + tap) * g.K + krow) * g.C + c;
+                    *reinterpret_cast<float4*>(o) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN))
+                     : "memory");
+    }
+}
+
 // Fixed-order sum over splits -> FilterKCRSblk (K, C) (P/include/spconv/tensor.hpp:112-119).
 __global__ void tc_bww_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dst, int splits, int K,
                                      int C, int R, int S, const int* __restrict__ nonfinite) {
@@ -1445,7 +1616,32 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
         return cudaErrorInvalidValue;
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
-    if (BN == 256)
+    // CTA pairs (two k tiles, half the D rows each) for single-tap 256-wide c tiles
+    static const int bpair_env = std::getenv("SPC_TC_PAIR") ? std::atoi(std::getenv("SPC_TC_PAIR")) : 1;
+    if (bpair_env && BN == 256 && tpc == 1 && g.ktiles % 2 == 0 && px == 1) {
+        CUtensorMap bhi2, blo2;
+        const int bB2[5] = {16, 128, 1, 1, 1};
+        if (!make_map5(&bhi2, d_hi, dD5, bB2) || !make_map5(&blo2, d_lo, dD5, bB2)) {
+            cudaFreeAsync(scratch, st);
+            return cudaErrorInvalidValue;
+        }
+        constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * 128 * 64;
+        constexpr int PST = 6;
+        const size_t smem = PST * STAGE + 1024 + 256;
+        static bool attr = false;
+        if (!attr) {
+            e = cudaFuncSetAttribute(tc_bww_pair_kernel<PST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) {
+                cudaFreeAsync(scratch, st);
+                return e;
+            }
+            attr = true;
+        }
+        dim3 grid((unsigned)(g.tgroups * g.ktiles * g.ctiles), (unsigned)g.splits);
+        tc_bww_pair_kernel<PST><<<grid, TC_THREADS, smem, st>>>(ahi, alo, bhi2, blo2, g, part, nonfinite, cnt, ex);
+        note_launch();
+        e = cudaGetLastError();
+    } else if (BN == 256)
         e = launch_bww_bn<256, 1>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);
     else if (BN == 192)
         e = launch_bww_bn<192, 1>(ahi, alo, bhi, blo, g, part, nonfinite, cnt, ex, st);

@@ -135,6 +135,7 @@ BWW_SHAPES = [
     (2, 512, 512, 7, 7, 3, 3),
     (20, 64, 64, 30, 17, 3, 3),
     (8, 128, 256, 14, 14, 1, 1),
+    (20, 256, 256, 13, 11, 3, 3),  # CTA-pair BWW (C >= 256, two k tiles), ragged images
 ]
 
 
