@@ -302,3 +302,35 @@ def test_tc_stride2_nonfinite_takes_exact_path(sp, R, comp):
     # 1x1 BWW is the GEMM kernel: same products, possibly another summation order
     assert O.max_abs_rel(tc[fin], f32[fin]) <= TC_TOL
     assert ctc == c32
+
+
+def test_tc_random_geometries_match_oracle(sp):
+    """Randomised sweep of the geometries the variant covers (odd and tiny
+    extents, 1..20 images, 64..256 channels, 3x3 / 1x1, stride 1 / 2), every
+    pass and both BWW check sides against the 64-bit oracle, counters exact."""
+    rng = np.random.default_rng(2024)
+    for trial in range(48):
+        N = int(rng.integers(1, 21))
+        C, K = (int(x) for x in rng.choice([64, 128, 192, 256], 2))
+        R = int(rng.choice([1, 3]))
+        O_ = int(rng.choice([1, 2]))
+        H, W = (int(x) for x in rng.integers(1, 21, 2))
+        sh = sp.ConvShape.make(N, C, K, H, W, R, R, O_, O_)
+        t = sh.astuple()
+        d = _gauss_relu(rng, (N, C, H, W), float(rng.uniform(0.3, 0.9)))
+        dy = _gauss_relu(rng, (N, K, sh.out_h(), sh.out_w()), float(rng.uniform(0.3, 0.9)))
+        g = (rng.standard_normal((K, C, R, R)) * np.sqrt(2.0 / (C * R * R))).astype(np.float32)
+        cases = [(0, 0, sp.pack_act_nchwc(d, V), sp.pack_filter(g, V), d, O.dense(0, t, d, g)),
+                 (1, 0, sp.pack_act_nchwc(dy, V), sp.pack_filter(g, V, True), dy, O.dense(1, t, dy, g))]
+        ref2 = O.dense(2, t, d, dy)
+        cases += [(2, 0, sp.pack_act_chwnn(d, V), sp.pack_act_nchwc(dy, V), d, ref2),
+                  (2, 1, sp.pack_act_nchwc(d, V), sp.pack_act_chwnn(dy, V), dy, ref2)]
+        for comp, check, a, b, mask, ref in cases:
+            pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
+            with sp.math_mode(sp.Math.tf32x3):
+                res = sp.run_parallel(a.to("cuda"), b.to("cuda"), sh, pl, sp.RunMode.sparse)
+            got = sp.unpack(res.out).cpu().numpy()
+            err = O.max_abs_rel(got, ref) if np.abs(ref).max() > 0 else float(np.abs(got).max())
+            assert err <= TC_TOL, (trial, t, comp, check, err)
+            want = O.expected_counts(t, O.plan(t, comp, V, 30, check), mask)
+            assert res.counters.executed_vector_fmas == want["executed_vector_fmas"], (trial, t, comp, check)
