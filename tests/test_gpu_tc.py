@@ -334,3 +334,29 @@ def test_tc_random_geometries_match_oracle(sp):
             assert err <= TC_TOL, (trial, t, comp, check, err)
             want = O.expected_counts(t, O.plan(t, comp, V, 30, check), mask)
             assert res.counters.executed_vector_fmas == want["executed_vector_fmas"], (trial, t, comp, check)
+
+
+def test_tc_host_buffer_path_matches_device_path(sp):
+    """The host-buffer drop-in (spc_run_parallel_host: chunked H2D / kernels /
+    D2H) under the tensor-core variant: FWD/BWI bitwise equal to the device
+    path (per-image tiles do not depend on the chunking), BWW (chunk partials
+    summed in fixed order) within the stated tolerance, counters equal."""
+    rng = np.random.default_rng(41)
+    sh = sp.ConvShape.make(40, 128, 256, 20, 18, 3, 3, 1, 1)
+    d = _gauss_relu(rng, (40, 128, 20, 18), 0.6)
+    dy = _gauss_relu(rng, (40, 256, 20, 18), 0.5)
+    g = (rng.standard_normal((256, 128, 3, 3)) * 0.03).astype(np.float32)
+    cases = [(0, 0, sp.pack_act_nchwc(d, V), sp.pack_filter(g, V)),
+             (1, 0, sp.pack_act_nchwc(dy, V), sp.pack_filter(g, V, True)),
+             (2, 0, sp.pack_act_chwnn(d, V), sp.pack_act_nchwc(dy, V))]
+    with sp.math_mode(sp.Math.tf32x3):
+        for comp, check, a, b in cases:
+            pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
+            rd = sp.run_parallel(a.to("cuda"), b.to("cuda"), sh, pl, sp.RunMode.sparse)
+            rh = sp.run_parallel(a, b, sh, pl, sp.RunMode.sparse)
+            gd = rd.out.data.cpu().numpy()
+            if comp < 2:
+                assert np.array_equal(rh.out.data, gd), comp
+            else:
+                assert O.max_abs_rel(rh.out.data, gd) <= TC_TOL
+            assert rh.counters == rd.counters
