@@ -872,6 +872,260 @@ cudaError_t launch_pair(const CUtensorMap& mhi, const CUtensorMap& mlo, const CU
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- 64-channel 3x3 halo kernel
+// tc_halo9_kernel (3x3 stride 1, BN = 64): the small-N tile is both L2-bound
+// (each tap reloads a shifted 128-pixel A box: VGG conv1_2 moved 13.6 TB/s
+// through L2 at 40% tensor-pipe activity) and MMA-issue-bound (6 short MMAs per
+// barrier round trip).  Here a stage is ONE 16-channel block: a halo box of
+// (RW + 2) rows x P pixels loaded once (the M = 128 rows are RW = 128 / P
+// output rows x pitch P, the last two columns of each row not outputs), plus
+// the filter slices of all 9 taps; the MMA issuer then runs 9 taps x 2 K steps
+// x 3 products = 54 MMAs on it, the A operand of tap (dv, du) being the 128
+// consecutive halo rows from row dv * P + du (the descriptor start moves by
+// 64-byte rows; SWIZZLE_64B keys on the address bits, so base offset 0).
+struct TcHalo9Geo {
+    int Ho, Wo, P, RW, tiles_x, tiles_y, RB, fwd, N, ntiles;
+    size_t out_img;
+};
+
+template <int P>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_halo9_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                    const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                    TcHalo9Geo g, float* __restrict__ dst, const int* __restrict__ nonfinite,
+                    const unsigned long long* __restrict__ cnt_tmp, unsigned long long* __restrict__ exec_ctr,
+                    Epi epi, const uint8_t* __restrict__ zflag) {
+    if (__ldg(nonfinite) != 0) return;
+    constexpr int BN = 64, RW = 128 / P, HALF = BN / 2;
+    constexpr uint32_t HROWS = (RW + 2) * P;                                // halo rows loaded
+    constexpr uint32_t A_HALF = ((HROWS + 8) * 64 + 1023) & ~1023u;       // + rows garbage columns read past it
+    constexpr uint32_t B_TAP = BN * 64;
+    constexpr uint32_t STAGE = 2 * A_HALF + 2 * 9 * B_TAP;
+    constexpr uint32_t STAGE_TX = 2 * HROWS * 64 + 2 * 9 * B_TAP;
+    constexpr int ST = 2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * STAGE);  // full[ST] empty[ST] tfull[2] tempty[2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
+    const uint32_t sbase = smem_u32(smem), bar0 = smem_u32(bars);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * ST + b); };
+    auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * ST + 2 + b); };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int txy = g.tiles_x * g.tiles_y;
+    const int NG = g.RB;
+    auto tile_coords = [&](int t, int& img, int& tt, int& x0, int& y0) {
+        img = t / txy;
+        tt = t - img * txy;
+        const int ty = tt / g.tiles_x;
+        x0 = (tt - ty * g.tiles_x) * (P - 2);
+        y0 = ty * RW;
+    };
+    auto live_mask = [&](int img, int tt) {
+        if (zflag == nullptr) return ~0ull;
+        unsigned long long m = 0;
+        for (int grp = 0; grp < NG; ++grp)
+            m |= (unsigned long long)(__ldg(zflag + ((size_t)img * NG + grp) * txy + tt) != 0) << grp;
+        return m;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (blockIdx.x == 0 && cnt_tmp && exec_ctr) atomicAdd(exec_ctr, *cnt_tmp);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(tmem_cols(2 * BN))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+            int gi = 0;
+            for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+                int img, tt, x0, y0;
+                tile_coords(t, img, tt, x0, y0);
+                const unsigned long long lm = live_mask(img, tt);
+                for (int rb = 0; rb < g.RB; ++rb) {
+                    if (!((lm >> rb) & 1ull)) continue;
+                    const int s = gi % ST;
+                    if (gi >= ST) mbar_wait(empty_bar(s), ((gi / ST) - 1) & 1);
+                    const uint32_t st = sbase + s * STAGE;
+                    mbar_expect_tx(full_bar(s), STAGE_TX);
+                    tma_load_5d(st, &map_hi, full_bar(s), 0, x0 - 1, y0 - 1, rb, img);
+                    tma_load_5d(st + A_HALF, &map_lo, full_bar(s), 0, x0 - 1, y0 - 1, rb, img);
+                    // shift (dv, du) reads source (y + dv - 1, x + du - 1): FWD tap (dv, du); BWI the
+                    // transposed filter's tap (2 - dv, 2 - du) (kernel_impl.hpp:85-89)
+                    for (int sft = 0; sft < 9; ++sft) {
+                        const int brow = (g.fwd ? sft : 8 - sft) * g.RB + rb;
+                        tma_load_3d(st + 2 * A_HALF + sft * B_TAP, &map_bhi, full_bar(s), 0, 0, brow);
+                        tma_load_3d(st + 2 * A_HALF + (9 + sft) * B_TAP, &map_blo, full_bar(s), 0, 0, brow);
+                    }
+                    ++gi;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tf32_idesc<BN>();
+            int gi = 0, sg = 0;
+            for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+                int img, tt, x0, y0;
+                tile_coords(t, img, tt, x0, y0);
+                const unsigned long long lm = live_mask(img, tt);
+                // one segment per channel block (54 MMAs)
+                for (int rb = 0; rb < g.RB; ++rb, ++sg) {
+                    if (!((lm >> rb) & 1ull)) {
+                        --sg;
+                        continue;
+                    }
+                    const int buf = sg & 1;
+                    if (sg >= 2) mbar_wait(tempty_bar(buf), ((sg >> 1) - 1) & 1);
+                    const int s = gi % ST;
+                    mbar_wait(full_bar(s), (gi / ST) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t st = sbase + s * STAGE;
+                    const uint32_t tm = tmem + buf * BN;
+#pragma unroll
+                    for (int sft = 0; sft < 9; ++sft) {
+                        const uint32_t aoff = (uint32_t)(((sft / 3) * P + (sft % 3)) * 64);
+                        const uint32_t bh = st + 2 * A_HALF + sft * B_TAP;
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const uint64_t ahi = sw64_desc(st + aoff + 32 * k);
+                            const uint64_t alo = sw64_desc(st + A_HALF + aoff + 32 * k);
+                            const uint64_t bhi = sw64_desc(bh + 32 * k);
+                            const uint64_t blo = sw64_desc(bh + 9 * B_TAP + 32 * k);
+                            umma_tf32(tm, alo, bhi, idesc, (sft == 0 && k == 0) ? 0u : 1u);
+                            umma_tf32(tm, ahi, blo, idesc, 1u);
+                            umma_tf32(tm, ahi, bhi, idesc, 1u);
+                        }
+                    }
+                    umma_commit(empty_bar(s));
+                    umma_commit(tfull_bar(buf));
+                    ++gi;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int m = q * 32 + lane;
+        const int py = m / P, px = m - py * P;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const size_t plane = (size_t)g.Ho * g.Wo * 16;
+        int sg = 0;
+        for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            int img, tt, x0, y0;
+            tile_coords(t, img, tt, x0, y0);
+            const unsigned long long lm = live_mask(img, tt);
+            float acc[HALF];
+#pragma unroll
+            for (int j = 0; j < HALF; ++j) acc[j] = 0.0f;
+            for (int rb = 0; rb < g.RB; ++rb) {
+                if (!((lm >> rb) & 1ull)) continue;
+                const int buf = sg & 1;
+                mbar_wait_sleep(tfull_bar(buf), (sg >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    float v[16];
+                    tmem_ld16(tmem + lane_off + buf * BN + h * HALF + 16 * j, v);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) acc[16 * j + e] += v[e];
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty_bar(buf));
+                ++sg;
+            }
+            const int y = y0 + py, x = x0 + px;
+            if (px < P - 2 && y < g.Ho && x < g.Wo) {
+                float* out = dst + (size_t)img * g.out_img + ((size_t)y * g.Wo + x) * 16;
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    float* o = out + (size_t)(h * (HALF / 16) + j) * plane;
+                    float v[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = acc[16 * j + e];
+                    if (epi.active()) {
+                        const size_t base = (size_t)(o - dst);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = epi.apply(v[e], base + e);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; e += 4)
+                        *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * 64))
+                     : "memory");
+    }
+}
+
+template <int P>
+cudaError_t launch_halo9(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUtensorMap& mbhi,
+                         const CUtensorMap& mblo, const TcHalo9Geo& g, float* dst, const int* nonfinite,
+                         const unsigned long long* cnt, unsigned long long* exec_ctr, const Epi& epi, cudaStream_t st,
+                         const uint8_t* zflag) {
+    constexpr int RW = 128 / P;
+    constexpr size_t A_HALF = (((size_t)(RW + 2) * P + 8) * 64 + 1023) & ~(size_t)1023;
+    constexpr size_t STAGE = 2 * A_HALF + 2 * 9 * 64 * 64;
+    const size_t smem = 2 * STAGE + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tc_halo9_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int ctas = 148;
+    if (ctas > g.ntiles) ctas = g.ntiles;
+    tc_halo9_kernel<P><<<ctas, TC_THREADS, smem, st>>>(mhi, mlo, mbhi, mblo, g, dst, nonfinite, cnt, exec_ctr, epi,
+                                                      zflag);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// Pitch for the halo kernel: P - 2 output columns per row, least padded area.
+int choose_pitch(int Ho, int Wo) {
+    long best = -1;
+    int bp = 64;
+    for (int P : {64, 32, 16}) {
+        const int rw = 128 / P;
+        const long area = (long)((Wo + P - 3) / (P - 2)) * P * ((Ho + rw - 1) / rw) * rw;
+        if (best < 0 || area < best) {
+            best = area;
+            bp = P;
+        }
+    }
+    return bp;
+}
+
 // ================================================================ BWW
 // dG[k, c, v, u] = sum_{i, y', x'} dY[i, k, y', x'] * D[i, c, y'+v-padH, x'+u-padW]
 // (P/src/kernel_impl.hpp:209-336, P/src/kernels.cpp:238-302), as one GEMM per
@@ -1483,6 +1737,39 @@ cudaError_t launch_tc_conv(bool fwd, bool sparse, const DevShape& sh, const floa
         note_launch();
     }
     unsigned long long* ex = (sparse && exec_ctr) ? exec_ctr : nullptr;
+    // 64-channel 3x3 stride-1 outputs: the halo kernel, one channel block (all 9
+    // taps) per stage (SPC_TC_HALO=0 disables)
+    static const int halo_env = std::getenv("SPC_TC_HALO") ? std::atoi(std::getenv("SPC_TC_HALO")) : 1;
+    if (halo_env && bn == 64 && Co == 64 && sh.R == 3 && sh.S == 3 && str == 1 && g.ncls == 1 && !ink) {
+        TcHalo9Geo hg;
+        hg.Ho = Ho;
+        hg.Wo = Wo;
+        hg.P = choose_pitch(Ho, Wo);
+        hg.RW = 128 / hg.P;
+        hg.tiles_x = (Wo + hg.P - 3) / (hg.P - 2);
+        hg.tiles_y = (Ho + hg.RW - 1) / hg.RW;
+        hg.RB = Cr / 16;
+        hg.fwd = fwd ? 1 : 0;
+        hg.N = sh.N;
+        hg.ntiles = sh.N * hg.tiles_x * hg.tiles_y;
+        hg.out_img = g.out_img;
+        CUtensorMap hhi, hlo;
+        if (!make_act_map(&hhi, src, sh.N, Cr / 16, Hs, Ws, hg.P, hg.RW + 2, 1) ||
+            !make_act_map(&hlo, lo, sh.N, Cr / 16, Hs, Ws, hg.P, hg.RW + 2, 1)) {
+            if (rowflag) cudaFreeAsync(rowflag, st);
+            cudaFreeAsync(scratch, st);
+            return cudaErrorInvalidValue;
+        }
+        // the zero-tile flags are per box tile of the generic geometry: not usable here
+        e = hg.P == 64   ? launch_halo9<64>(hhi, hlo, mbhi, mblo, hg, dst, nonfinite, cnt, ex, epi, st, nullptr)
+            : hg.P == 32 ? launch_halo9<32>(hhi, hlo, mbhi, mblo, hg, dst, nonfinite, cnt, ex, epi, st, nullptr)
+                         : launch_halo9<16>(hhi, hlo, mbhi, mblo, hg, dst, nonfinite, cnt, ex, epi, st, nullptr);
+        if (e == cudaSuccess)
+            e = launch_tile_conv_when(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, nonfinite, 1);
+        if (rowflag) cudaFreeAsync(rowflag, st);
+        cudaFreeAsync(scratch, st);
+        return e;
+    }
     // CTA pairs (SPC_TC_PAIR=0 disables): 3x3 / 1x1 without the in-smem split,
     // one output class, one block per stage
     static const int pair_env = std::getenv("SPC_TC_PAIR") ? std::atoi(std::getenv("SPC_TC_PAIR")) : 1;
