@@ -190,14 +190,31 @@ __device__ __forceinline__ void jt_words(Acc& acc, const Gv& g, const float* vv,
 // table when the previous block's measured density (nonzeros / region
 // pixels, summed over the CTA's warps) is at most JT%, else per-pixel
 // branches.  All variants accumulate in the same order (bitwise identical).
+#ifndef SPC_TILE_MAXREG
+#define SPC_TILE_MAXREG 236
+#endif
+#ifndef SPC_TILE_MAXREG_JT
+#define SPC_TILE_MAXREG_JT 228
+#endif
+// Register caps for the two sparse 3x3 s1 kernels that launch_tile_conv runs
+// on 128-channel layers (KK=4 7x4 branches, KK=4 4x8 jump table), applied
+// through tile_conv_kernel_capped.  They change no occupancy (2 warps per SM
+// sub-partition either way: 16K registers each), only ptxas's allocation and
+// schedule; measured on the VGG16 b32 sweep.  0 = no cap.
+constexpr int tile_maxreg(int nt, int kk, int th, int tw, int r, int str, int jt) {
+    return (r != 3 || str != 1 || kk != 4)        ? 0
+           : (nt == 32 && th * tw == 28 && jt == 0) ? SPC_TILE_MAXREG
+           : (th * tw == 32 && jt == 100)          ? SPC_TILE_MAXREG_JT
+                                                   : 0;
+}
+
 template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF, int JT, bool SPARSE,
           bool EPI>
-__global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, const float* __restrict__ src,
-                                                                   const float* __restrict__ filt,
-                                                                   float* __restrict__ dst,
-                                                                   unsigned long long* __restrict__ exec_ctr,
-                                                                   const int* __restrict__ sel, int want,
-                                                                   int group_fastest, Epi epi, Gate gate) {
+__device__ __forceinline__ void tile_conv_body(DevShape sh, const float* __restrict__ src,
+                                               const float* __restrict__ filt, float* __restrict__ dst,
+                                               unsigned long long* __restrict__ exec_ctr,
+                                               const int* __restrict__ sel, int want, int group_fastest, Epi epi,
+                                               Gate gate) {
     using Gm = ConvGeom<FWD, KK, TH, TW, NWY, NWX, R, S, STR>;
     // device-side kernel choice (see launch_tile_conv): the variant whose
     // selector value does not match exits before touching memory
@@ -489,6 +506,35 @@ __global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(DevShape sh, 
     gate.finish(blockIdx.y);
 }
 
+#define SPC_TC_TPARAMS                                                                                          \
+    bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF, int JT, bool SPARSE, bool EPI
+#define SPC_TC_TARGS FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, SPARSE, EPI
+#define SPC_TC_ARGS                                                                                             \
+    DevShape sh, const float* __restrict__ src, const float* __restrict__ filt, float* __restrict__ dst,         \
+        unsigned long long* __restrict__ exec_ctr, const int* __restrict__ sel, int want, int group_fastest, Epi epi, \
+        Gate gate
+template <SPC_TC_TPARAMS>
+__global__ void __launch_bounds__(NWY * NWX * 32) tile_conv_kernel(SPC_TC_ARGS) {
+    tile_conv_body<SPC_TC_TARGS>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest, epi, gate);
+}
+// the same kernel under a register cap (tile_maxreg); separate so the
+// uncapped instantiations keep ptxas's own allocation
+template <SPC_TC_TPARAMS>
+__global__ void __launch_bounds__(NWY * NWX * 32) __maxnreg__(tile_maxreg(NWY * NWX * 32, KK, TH, TW, R, STR, JT) > 0 ? tile_maxreg(NWY * NWX * 32, KK, TH, TW, R, STR, JT) : 255)
+    tile_conv_kernel_capped(SPC_TC_ARGS) {
+    tile_conv_body<SPC_TC_TARGS>(sh, src, filt, dst, exec_ctr, sel, want, group_fastest, epi, gate);
+}
+template <SPC_TC_TPARAMS>
+constexpr auto tile_conv_entry() {
+    if constexpr (SPARSE && tile_maxreg(NWY * NWX * 32, KK, TH, TW, R, STR, JT) > 0)
+        return tile_conv_kernel_capped<SPC_TC_TARGS>;
+    else
+        return tile_conv_kernel<SPC_TC_TARGS>;
+}
+#undef SPC_TC_TPARAMS
+#undef SPC_TC_TARGS
+#undef SPC_TC_ARGS
+
 // ---------------------------------------------------------------- dispatch
 template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF = 1, int JT = 0,
           bool WITH_EPI = false>
@@ -507,13 +553,13 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
     const bool with_epi = epi.active();
     if (with_epi) {
         if constexpr (WITH_EPI)
-            kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, true>
-                          : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, true>;
+            kern = sparse ? tile_conv_entry<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, true>()
+                          : tile_conv_entry<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, true>();
         else
             return cudaErrorInvalidValue;
     } else {
-        kern = sparse ? tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, false>
-                      : tile_conv_kernel<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, false>;
+        kern = sparse ? tile_conv_entry<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, false>()
+                      : tile_conv_entry<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, false>();
     }
     static bool attr_set[2][2] = {{false, false}, {false, false}};  // per instantiation: [epi][sparse]
     if (!attr_set[with_epi][sparse]) {
@@ -697,7 +743,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
         // resolution; KK=4 branches for sparse, the KK=4 4x8 jump table for
-        // density <= 15%, KK=2 7x7 for dense mode.
+        // density <= 24% (measured crossover between s = 0.7 and 0.8 under the
+        // register caps), KK=2 7x7 for dense mode.
         if (sparse && kk4) {
             const int Ci = fwd ? sh.C : sh.K;
             const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
@@ -706,7 +753,7 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             if (e != cudaSuccess) return e;
             // gated (host-buffer) launches sample only the first input chunk
             const size_t per_img = (size_t)Ci * Hs * Ws;
-            launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 15, sel, st, gate);
+            launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 24, sel, st, gate);
             e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate)
                     : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate);
             if (e == cudaSuccess)
