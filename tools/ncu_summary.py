@@ -12,7 +12,7 @@ def family(name):
     n = re.sub(r"[<(].*", "", name).replace("void ", "").strip()
     m = re.search(r"<([^>]*)>\(", name)
     args = [a.strip().replace("(bool)", "").replace("(int)", "") for a in m.group(1).split(",")] if m else []
-    if args and n.endswith("tile_conv_kernel"):
+    if args and n.endswith(("tile_conv_kernel", "tile_conv_kernel_capped")):
         # <FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, SPARSE, EPI>
         sparse = args[11] if len(args) > 12 else args[-1]
         jt = args[10] if len(args) > 10 else "0"
