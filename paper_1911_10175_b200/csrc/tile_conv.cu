@@ -196,16 +196,22 @@ __device__ __forceinline__ void jt_words(Acc& acc, const Gv& g, const float* vv,
 #ifndef SPC_TILE_MAXREG_JT
 #define SPC_TILE_MAXREG_JT 228
 #endif
-// Register caps for the two sparse 3x3 s1 kernels that launch_tile_conv runs
-// on 128-channel layers (KK=4 7x4 branches, KK=4 4x8 jump table), applied
-// through tile_conv_kernel_capped.  They change no occupancy (2 warps per SM
-// sub-partition either way: 16K registers each), only ptxas's allocation and
-// schedule; measured on the VGG16 b32 sweep.  0 = no cap.
+// Register caps for sparse 3x3 s1 kernels of launch_tile_conv, applied
+// through tile_conv_kernel_capped.  KK=4 7x4 branches (236) and KK=4 4x8 jump
+// table (228): no occupancy change (2 warps per SM sub-partition either way:
+// 16K registers each), only ptxas's allocation and schedule.  KK=2 4x8 jump
+// table (128, from 166): 4 warps per sub-partition instead of 3.  Measured on
+// the VGG16 b32 sweep.  0 = no cap.
+#ifndef SPC_TILE_MAXREG_JT2
+#define SPC_TILE_MAXREG_JT2 128
+#endif
 constexpr int tile_maxreg(int nt, int kk, int th, int tw, int r, int str, int jt) {
-    return (r != 3 || str != 1 || kk != 4)        ? 0
-           : (nt == 32 && th * tw == 28 && jt == 0) ? SPC_TILE_MAXREG
-           : (th * tw == 32 && jt == 100)          ? SPC_TILE_MAXREG_JT
-                                                   : 0;
+    return (r != 3 || str != 1)                            ? 0
+           : (kk == 2 && th * tw == 32 && jt == 100)        ? SPC_TILE_MAXREG_JT2
+           : (kk != 4)                                     ? 0
+           : (nt == 32 && th * tw == 28 && jt == 0)         ? SPC_TILE_MAXREG
+           : (th * tw == 32 && jt == 100)                  ? SPC_TILE_MAXREG_JT
+                                                           : 0;
 }
 
 template <bool FWD, int KK, int TH, int TW, int NWY, int NWX, int R, int S, int STR, int GPF, int JT, bool SPARSE,
@@ -759,6 +765,26 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             if (e == cudaSuccess)
                 e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
                         : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
+            cudaFreeAsync(sel, st);
+            return e;
+        }
+        if (sparse && xsel == nullptr) {
+            // 64-channel multiples: the KK=2 branch kernel, or below 21% density
+            // its jump-table twin on the same 8x16 CTA tile (capped at 128
+            // registers: 4 CTAs per SM; conv1_2 s=0.9 87 vs 64 TF/s, s=0.8 64 vs
+            // 62.5, s=0.6 44 vs 59)
+            const int Ci = fwd ? sh.C : sh.K;
+            const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
+            int* sel = nullptr;
+            cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
+            if (e != cudaSuccess) return e;
+            const size_t per_img = (size_t)Ci * Hs * Ws;
+            launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 21, sel, st, gate);
+            e = fwd ? launch_cfg<true, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate)
+                    : launch_cfg<false, 2, 4, 8, 2, 2, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate);
+            if (e == cudaSuccess)
+                e = fwd ? launch_cfg<true, 2, 4, 8, 2, 2, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
+                        : launch_cfg<false, 2, 4, 8, 2, 2, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
             cudaFreeAsync(sel, st);
             return e;
         }

@@ -374,13 +374,16 @@ def test_jump_table_and_branch_kernels_agree_bitwise(sp):
     import torch
     V = 16
     L = sp._lib.load()
-    sh = sp.ConvShape.make(2, 128, 128, 20, 22, 3, 3, 1, 1)
-    for comp in (0, 1):
+    # (2, 17): KK=4 4x8 tile, branches vs jump table; (6, 14): the KK=2 8x16 CTA pair
+    # that launch_tile_conv runs on 64-channel multiples
+    for C_, variants in ((128, (2, 17)), (64, (6, 14))):
+      sh = sp.ConvShape.make(2, C_, C_, 20, 22, 3, 3, 1, 1)
+      for comp in (0, 1):
         for s in (0.5, 0.95):
             a, b, ba, bb = make_inputs(sp, sh, comp, 0, s, V, 77)
             pl = sp.plan(sh, sp.Component(comp), V)
             outs = []
-            for variant in (2, 17):  # same tile (KK=4, 4x8), branches vs jump table
+            for variant in variants:
                 out = torch.empty(sh.N * (sh.K if comp == 0 else sh.C) * (sh.out_h() if comp == 0 else sh.H)
                                   * (sh.out_w() if comp == 0 else sh.W), device="cuda")
                 cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
