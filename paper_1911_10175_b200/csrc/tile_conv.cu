@@ -748,7 +748,7 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
     if (sh.R == 3 && sh.O == 1) {
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
-        // resolution; KK=4 branches for sparse, the KK=4 4x8 jump table for
+        // resolution; KK=4 branches for sparse, the KK=4 4x8 one-warp jump table for
         // density <= 24% (measured crossover between s = 0.7 and 0.8 under the
         // register caps), KK=2 7x7 for dense mode.
         if (sparse && kk4) {
@@ -763,8 +763,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate)
                     : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate);
             if (e == cudaSuccess)
-                e = fwd ? launch_cfg<true, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
-                        : launch_cfg<false, 4, 4, 8, 2, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
+                e = fwd ? launch_cfg<true, 4, 4, 8, 1, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
+                        : launch_cfg<false, 4, 4, 8, 1, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
             cudaFreeAsync(sel, st);
             return e;
         }
