@@ -374,9 +374,10 @@ def test_jump_table_and_branch_kernels_agree_bitwise(sp):
     import torch
     V = 16
     L = sp._lib.load()
-    # (2, 17): KK=4 4x8 tile, branches vs jump table; (6, 14): the KK=2 8x16 CTA pair
-    # that launch_tile_conv runs on 64-channel multiples
-    for C_, variants in ((128, (2, 17)), (64, (6, 14))):
+    # 128 channels: the production branch kernel (42, KK=4 7x4), branches on a 4x8 tile (2), the
+    # 2-warp (17) and the production one-warp (41) jump tables; 64 channels: the KK=2 8x16 CTA pair
+    # that launch_tile_conv runs on 64-channel multiples (6 branches, 14 jump table)
+    for C_, variants in ((128, (42, 2, 17, 41)), (64, (6, 14))):
       sh = sp.ConvShape.make(2, C_, C_, 20, 22, 3, 3, 1, 1)
       for comp in (0, 1):
         for s in (0.5, 0.95):
@@ -395,8 +396,9 @@ def test_jump_table_and_branch_kernels_agree_bitwise(sp):
                 assert st == 0, sp._lib.last_error()
                 torch.cuda.synchronize()
                 outs.append((out.cpu().numpy(), cnt.cpu().numpy()))
-            assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
-            assert np.array_equal(outs[0][1], outs[1][1])
+            for o in outs[1:]:
+                assert np.array_equal(outs[0][0].view(np.uint32), o[0].view(np.uint32))
+                assert np.array_equal(outs[0][1], o[1])
 
 
 def test_cxx_dropin_matches_reference_library():
