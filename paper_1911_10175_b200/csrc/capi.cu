@@ -799,9 +799,11 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     cudaStream_t s0 = hs->s[0];
     // SPC_HOST_GATE=1 selects the single gated launch for FWD/BWI.  Measured on
     // the VGG16 step it is not faster than the chunked path (0.577 vs 0.562 s:
-    // PCIe-bound either way), so the chunked path is the default.
+    // PCIe-bound either way), so the chunked path is the default.  The gated
+    // launch is an FFMA tile kernel: the tensor-core arithmetic keeps the
+    // chunked path, so the host and device paths compute alike.
     static const bool gate_on = std::getenv("SPC_HOST_GATE") && std::atoi(std::getenv("SPC_HOST_GATE")) == 1;
-    if (plan->comp != SPC_BWW && gate_on &&
+    if (plan->comp != SPC_BWW && gate_on && math_mode() == SPC_MATH_FP32 &&
         conv_supports_gate(plan->comp == SPC_FWD, make_dev_shape(*shape), plan->V)) {
         st = run_fwd_bwi_gated(plan->comp == SPC_FWD, a, b, *shape, *plan, mode, out, counters, hs);
         if (st == SPC_OK) *dst = out;
