@@ -6,6 +6,8 @@ Stated tolerance of the variant: max|got - ref| / max|ref|
 ~2^-21 relative error, measured ~1e-7 here.  Counters (executed_vector_fmas,
 checked_vectors) stay integer-exact; Inf/NaN inputs take the exact FFMA path.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -185,7 +187,12 @@ def test_tc_bww_nonfinite_takes_exact_path(sp):
     (f32, c32), (tc, ctc) = outs
     assert np.array_equal(np.isnan(tc), np.isnan(f32)) and np.array_equal(np.isinf(tc), np.isinf(f32))
     fin = np.isfinite(f32)
-    assert np.array_equal(tc[fin], f32[fin])
+    if os.environ.get("SPC_FORCE_GENERIC") == "1":
+        # A/B knob: the FP32 run took the shape-general kernel, whose reduction
+        # order differs from the tile BWW behind the tensor-core fallback
+        assert O.max_abs_rel(tc[fin], f32[fin]) <= TC_TOL
+    else:
+        assert np.array_equal(tc[fin], f32[fin])
     assert ctc == c32
 
 
