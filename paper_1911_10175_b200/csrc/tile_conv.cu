@@ -749,8 +749,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
         // tile choices from tools/tune.py sweeps over the VGG16 layers
         // (profiles/r01_tune.md): 7-wide tiles divide every VGG/ResNet
         // resolution; KK=4 branches for sparse, the KK=4 4x8 one-warp jump table for
-        // density <= 24% (measured crossover between s = 0.7 and 0.8 under the
-        // register caps), KK=2 7x7 for dense mode.
+        // density <= 28% (measured crossover near s = 0.7 for the capped one-warp
+        // jump table: s = 0.75 3-9% ahead, s = 0.7 even), KK=2 7x7 for dense mode.
         if (sparse && kk4) {
             const int Ci = fwd ? sh.C : sh.K;
             const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
@@ -759,7 +759,7 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             if (e != cudaSuccess) return e;
             // gated (host-buffer) launches sample only the first input chunk
             const size_t per_img = (size_t)Ci * Hs * Ws;
-            launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 24, sel, st, gate);
+            launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 28, sel, st, gate);
             e = fwd ? launch_cfg<true, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate)
                     : launch_cfg<false, 4, 7, 4, 1, 1, 3, 3, 1, 1, 0, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 0, epi, gate);
             if (e == cudaSuccess)
