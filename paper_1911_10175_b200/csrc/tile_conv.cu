@@ -190,18 +190,19 @@ __device__ __forceinline__ void jt_words(Acc& acc, const Gv& g, const float* vv,
 // table when the previous block's measured density (nonzeros / region
 // pixels, summed over the CTA's warps) is at most JT%, else per-pixel
 // branches.  All variants accumulate in the same order (bitwise identical).
-#ifndef SPC_TILE_MAXREG
-#define SPC_TILE_MAXREG 244
-#endif
-#ifndef SPC_TILE_MAXREG_JT
-#define SPC_TILE_MAXREG_JT 228
-#endif
+
 // Register caps for sparse 3x3 s1 kernels of launch_tile_conv, applied
 // through tile_conv_kernel_capped.  KK=4 7x4 branches (244) and KK=4 4x8 jump
 // table (228): no occupancy change (2 warps per SM sub-partition either way:
 // 16K registers each), only ptxas's allocation and schedule.  KK=2 4x8 jump
 // table (128, from 166): 4 warps per sub-partition instead of 3.  Measured on
 // the VGG16 b32 sweep.  0 = no cap.
+#ifndef SPC_TILE_MAXREG
+#define SPC_TILE_MAXREG 244
+#endif
+#ifndef SPC_TILE_MAXREG_JT
+#define SPC_TILE_MAXREG_JT 228
+#endif
 #ifndef SPC_TILE_MAXREG_JT2
 #define SPC_TILE_MAXREG_JT2 128
 #endif
