@@ -433,7 +433,14 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
     const int Lc = CI ? sh.K : sh.C, Mc = CI ? sh.C : sh.K;
     const long items = (long)((sh.N + 15) / 16) * ((sh.Wp + TW - 1) / TW) * ((sh.Hp + TH - 1) / TH);
     const long base = (long)(Mc / G::NCH) * (Lc / (32 * KK));
-    long splits = (148L * 6 + base - 1) / base;
+    // Split count: aim for ~6 CTAs per SM; 3x3 s1 layers with 16-128 base
+    // CTAs (VGG conv2_2..conv4_1) measured 4-10% faster at ~18 per SM
+    // (SPC_BWW_CTAS sweep, profiles/r01_tune.md).  Fixed per shape, so the
+    // summation order stays deterministic.
+    static const long env_ctas = std::getenv("SPC_BWW_CTAS") ? std::atol(std::getenv("SPC_BWW_CTAS")) : 0;
+    const long target_ctas =
+        env_ctas > 0 ? env_ctas : (R == 3 && STR == 1 && base >= 16 && base <= 128) ? 148L * 18 : 148L * 6;
+    long splits = (target_ctas + base - 1) / base;
     if (splits > items) splits = items;
     if (splits < 1) splits = 1;
     const size_t E = (size_t)Mc * R * S * Lc;
