@@ -119,32 +119,72 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference arm
-def reference_sample(layers, grid, n_img, workers, seed=0):
-    """Time the unmodified reference CPU library (run_parallel, backend
-    automatic, `workers` threads) on a batch slice of every layer and sparsity.
-    Returns (dense-equiv flops, seconds)."""
-    import numpy as np
+# Everything on this arm runs the UNMODIFIED reference library (oracle/_ref,
+# built from /root/reference's sources by oracle/Makefile) through its public
+# API: shapes from the reference's conv_shape::make (P/src/tensor.cpp:11-14),
+# operands packed by the reference (pack_act_* / pack_filter), the timed call
+# spconv::run_parallel (P/src/kernels.cpp:304-313) with backend automatic and
+# every host thread.  It never loads the product library: the layer table and
+# the input generators are plain numpy (workloads.SPECS / *_host).
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
+
+def ref_layers(config, n_img=None):
+    """[(name, PlainShape)] of `config`, built by the reference's own conv_shape::make."""
     import oracle
     from paper_1911_10175_b200 import workloads as wl
-    rng = np.random.default_rng(seed)
-    flops = 0.0
-    secs = 0.0
+    out = []
+    for name, N, C, K, hw, R, stride in wl.SPECS[config]():
+        t = oracle.ref_shape_make(n_img or N, C, K, hw, hw, R, R, stride, stride)
+        out.append((name, wl.PlainShape(t)))
+    return out
+
+
+def reference_sample(config, grid, n_img, workers, mode=0, seed=0, passes=(0, 1, 2)):
+    """Time the reference's run_parallel on `n_img` images of every layer of
+    `config` at each sparsity of `grid` (FWD, BWI, BWW check = input, as the
+    reference's own sweep, P/src/bench.cpp:228).  Inputs: the config's
+    distributions (workloads.layer_inputs_host).  Returns (dense-equiv flops,
+    seconds inside run_parallel)."""
+    import oracle
+    from paper_1911_10175_b200 import workloads as wl
+    flops = secs = 0.0
     for s in grid:
-        for layer in layers:
-            sh = layer.shape.with_batch(n_img)
-            t = sh.astuple()
-            D = wl.host_activation((sh.N, sh.C, sh.H, sh.W), s, rng)
-            G = wl.host_weights(sh.K, sh.C, sh.S, sh.R, rng)
-            dY = wl.host_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), s, rng)
-            for comp, a, b in ((0, D, G), (1, dY, G), (2, D, dY)):
-                r = oracle.RefRun(comp, 0, t, 16, a, b)
+        for li, (name, sh) in enumerate(ref_layers(config, n_img)):
+            D, G, dY = wl.layer_inputs_host(config, li, sh, s, seed=seed)
+            for comp in passes:
+                a, b = ((D, G), (dY, G), (D, dY))[comp]
+                r = oracle.RefRun(comp, 0, sh.astuple(), 16, a, b)
                 t0 = time.perf_counter()
-                r.exec(0, workers)  # run_parallel: the reference's timed call (bench.cpp:249-271)
+                r.exec(mode, workers)  # run_parallel: the reference's timed call (bench.cpp:249-271)
                 secs += time.perf_counter() - t0
                 flops += sh.dense_flops()
                 r.close()
     return flops, secs
+
+
+def ref_images(config):
+    """Reference-arm sample per layer: one full 16-image ActCHWNn lane block
+    (the BWW check tensor's N lanes are all live), or the whole batch when smaller."""
+    from paper_1911_10175_b200 import workloads as wl
+    return min(16, wl.SPECS[config]()[0][1])
+
+
+def ref_grid(config, grid):
+    from paper_1911_10175_b200 import workloads as wl
+    return list(grid) if config in wl.GRID_CONFIGS else [None]
+
+
+def assert_product_not_loaded():
+    maps = open("/proc/self/maps").read()
+    assert "libspconv_b200" not in maps, "reference arm loaded the product library"
 
 
 def run_reference_arm(args):
@@ -152,30 +192,34 @@ def run_reference_arm(args):
     if rank != 0:
         return
     import oracle
-    from paper_1911_10175_b200 import workloads as wl
     if not oracle.ref_available():
         emit({"impl": "reference", "unavailable": "oracle/_ref/libspconv_ref.so was not built"})
         return
-    layers = wl.CONFIGS[args.config]()
     workers = os.cpu_count() or 1
-    n_img = args.ref_images
-    for _ in range(args.warmup):
-        reference_sample(layers, args.grid[:1], n_img, workers)
+    n_img = args.ref_images or ref_images(args.config)
+    grid = ref_grid(args.config, args.grid)
+    # one step = every layer x FWD/BWI/BWW at ONE sparsity of the grid
+    # (rotating through the grid step by step), n_img images per layer
+    for k in range(args.warmup):
+        reference_sample(args.config, [grid[k % len(grid)]], n_img, workers, seed=100 + k)
     tot_f = tot_s = 0.0
     for k in range(args.steps):
-        f, s = reference_sample(layers, args.grid, n_img, workers, seed=k)
+        f, s = reference_sample(args.config, [grid[k % len(grid)]], n_img, workers, seed=k)
         tot_f += f
         tot_s += s
+    assert_product_not_loaded()
     value = tot_f / tot_s / 1e9
-    sample = (f"{n_img} image(s) of batch {layers[0].shape.N} x {len(layers)} layers x FWD/BWI/BWW x sparsity "
-              f"{list(args.grid)}; run_parallel (P/src/kernels.cpp:304), backend automatic")
+    n_full = ref_layers(args.config)[0][1].N
+    sample = (f"{n_img} of {n_full} images x {len(ref_layers(args.config))} layers x FWD/BWI/BWW per step, "
+              f"sparsity rotating over {grid} step by step; run_parallel (P/src/kernels.cpp:304), backend "
+              f"automatic, {workers} threads; CPU: {cpu_model()}")
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(tot_s / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(args, ws), "impl": "reference",
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": workers, "kind": "reference",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(out)
@@ -192,35 +236,101 @@ WORKLOAD_NAMES = {
 
 def config_dict(args, ws):
     from paper_1911_10175_b200 import workloads as wl
-    n = wl.CONFIGS[args.config]()[0].shape.N
+    from paper_1911_10175_b200.dist import shard_range
+    n = wl.SPECS[args.config]()[0][1]
+    per = [shard_range(n, ws, r)[1] for r in range(ws)]
     return {"workload": f"{args.config}: {WORKLOAD_NAMES.get(args.config, args.config)}",
-            "global_batch": n * ws, "per_gpu_batch": n, "resolution": 224, "vector_width": 16,
-            "sparsity_grid": list(args.grid), "bww_check": "input",
-            "parallelism": f"dp{ws} (batch-sharded, BWW dG allreduce)",
-            "l2": "inputs larger than L2 (step working set ~25 GB, each tensor touched once per step)"}
+            "global_batch": n, "per_gpu_batch": per[0] if min(per) == max(per) else per,
+            "resolution": 224, "vector_width": 16,
+            "sparsity": (list(args.grid) if args.config in wl.GRID_CONFIGS else SPARSITY_NOTE.get(args.config)),
+            "bww_check": "input",
+            "parallelism": f"dp{ws} (global batch sharded over ranks, BWW dG NCCL allreduce)",
+            "l2": "inputs larger than L2 (step working set > 1 GB, each tensor touched once per step)"}
+
+
+SPARSITY_NOTE = {
+    "resnet34_b64": "D: per-layer i.i.d. s_l ~ U[0.4, 0.8] (seeded); dY dense (BatchNorm)",
+    "resnet50_b64": "D: spatially correlated ReLU(conv3x3_rand(N(0,1)) - tau), mean 0.6; dY dense (BatchNorm)",
+    "fixup_resnet50_b256": "ReLU masks of the chain's own seeded forward pass (~0.7 activation sparsity)",
+}
 
 
 # ---------------------------------------------------------------- our arm
+def relaunch_distributed(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-exec this script as N
+    ranks under torch.distributed.run (one process per GPU, 127.0.0.1
+    rendezvous); the rank-0 child prints the JSON line on our stdout."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"--gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+    log("relaunch:", " ".join(cmd))
+    return subprocess.run(cmd, env=env, stdout=_RESULT_FD).returncode
+
+
+def build_work(args, sp, wl, dev, n_local, rank, dg_alloc):
+    """Resident inputs and prepared passes of one step on this rank's batch
+    shard: [(tag, layer_idx, pass, PreparedPass, global dense flops, dG buf)]."""
+    import torch
+    V = 16
+    specs = wl.SPECS[args.config]()
+    grid = list(args.grid) if args.config in wl.GRID_CONFIGS else [None]
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    work = []
+    for s in grid:
+        for li, spec in enumerate(specs):
+            gsh = sp.ConvShape.make(spec[1], spec[2], spec[3], spec[4], spec[4], spec[5], spec[5], spec[6], spec[6])
+            sh = gsh.with_batch(n_local)
+            D, G, dY = wl.layer_inputs_device(args.config, li, sh, gen, s)
+            bD = sp.pack_act_nchwc(D, V)
+            bDc = sp.nchwc_to_chwnn(bD)
+            bY = sp.pack_act_nchwc(dY, V)
+            del D, dY
+            ops = {"fwd": (bD, sp.pack_filter(G, V)), "bwi": (bY, sp.pack_filter(G, V, True)), "bww": (bDc, bY)}
+            tag = f"{s:.1f}" if s is not None else "cfg"
+            for name in PASSES:
+                a, b = ops[name]
+                pl = sp.plan(sh, sp.Component[name], V, 30, sp.BwwCheck.input)
+                cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+                out = dg_alloc(gsh.K * gsh.C * gsh.R * gsh.S) if name == "bww" else None
+                pp = sp.PreparedPass(a, b, sh, pl, sp.RunMode.sparse, out=out, counters=cnt)
+                work.append((tag, li, name, pp, gsh.dense_flops(), out))
+    return work
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="vgg16_b32")
+    ap.add_argument("--config", default="vgg16_b32", choices=sorted(WORKLOAD_NAMES))
     ap.add_argument("--grid", type=float, nargs="+", default=list(GRID))
-    ap.add_argument("--ref-images", type=int, default=1, help="reference-arm batch slice per layer")
-    ap.add_argument("--cpu-images", type=int, default=8, help="cpu_baseline batch slice per layer")
+    ap.add_argument("--ref-images", type=int, default=0,
+                    help="reference-arm images per layer (0: one full 16-image lane block)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tc", action="store_true", help="skip the 3xTF32 tensor-core variant")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs' lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
 
     import numpy as np
     import torch
@@ -228,67 +338,69 @@ def main():
 
     import paper_1911_10175_b200 as sp
     from paper_1911_10175_b200 import workloads as wl
+    from paper_1911_10175_b200.dist import Comm, shard_range
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # under torchrun (any world size) the collective path is live: NCCL
-    # process group, per-layer dG allreduce on a comm stream, barriers and
-    # max-over-ranks timing -- so a 1-GPU torchrun run exercises it too
+    # under torchrun (any world size) the collective path is live: the
+    # product's NCCL communicator (csrc/comm.cu) with dG in a symmetric window,
+    # per-layer allreduce on a comm stream, barriers, max-over-ranks timing
     distributed = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
+    comm = None
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
+        comm = Comm()
+        log(f"[rank {rank}] spc_comm: {comm.size} ranks, NCCL {sp._lib.load().spc_nccl_version()}")
     V = 16
-    layers = wl.CONFIGS[args.config]()
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
+    N_global = wl.SPECS[args.config]()[0][1]
+    _, n_local = shard_range(N_global, ws, rank)
+
+    if args.config == "fixup_resnet50_b256":
+        return run_chain_bench(args, sp, dev, stream, ws, rank, local, comm, distributed)
 
     # ---------------- setup: resident inputs, prepared passes (untimed)
-    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    work = []  # (s, layer_idx, pass, PreparedPass, dense_flops)
-    dgs = []   # (s, layer_idx, dG tensor) for the allreduce
     t_setup = time.time()
-    for s in args.grid:
-        for li, layer in enumerate(layers):
-            sh = layer.shape
-            G = wl.device_weights(sh.K, sh.C, sh.S, sh.R, gen)
-            D = wl.device_activation((sh.N, sh.C, sh.H, sh.W), s, gen)
-            dY = wl.device_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), s, gen)
-            bD = sp.pack_act_nchwc(D, V)
-            bDc = sp.nchwc_to_chwnn(bD)
-            bY = sp.pack_act_nchwc(dY, V)
-            del D, dY
-            ops = {"fwd": (bD, sp.pack_filter(G, V)), "bwi": (bY, sp.pack_filter(G, V, True)), "bww": (bDc, bY)}
-            for name in PASSES:
-                a, b = ops[name]
-                pl = sp.plan(sh, sp.Component[name], V, 30, sp.BwwCheck.input)
-                cnt = torch.zeros(4, dtype=torch.int64, device=dev)
-                pp = sp.PreparedPass(a, b, sh, pl, sp.RunMode.sparse, counters=cnt)
-                work.append((s, li, name, pp, sh.dense_flops()))
-                if name == "bww":
-                    dgs.append((s, li, pp.out))
-    torch.cuda.synchronize()
-    log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s, {len(work)} passes/step, "
-        f"{torch.cuda.memory_allocated(dev) / 2**30:.1f} GiB resident")
+    specs = wl.SPECS[args.config]()
+    grid = list(args.grid) if args.config in wl.GRID_CONFIGS else [None]
+    dg_total = len(grid) * sum(t[2] * t[3] * t[5] * t[5] for t in specs)
+    symmetric = False
+    if comm is not None:
+        dg_buf, symmetric = comm.window(dg_total)
+    else:
+        dg_buf = torch.empty(dg_total, dtype=torch.float32, device=dev)
+    cursor = [0]
 
-    comm_stream = torch.cuda.Stream(device=dev) if distributed else None
+    def dg_alloc(n):
+        start = cursor[0]
+        cursor[0] += n
+        return dg_buf.slice(start, n) if comm is not None else dg_buf[start:start + n]
+
+    work = build_work(args, sp, wl, dev, n_local, rank, dg_alloc)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] setup {time.time() - t_setup:.1f}s, {len(work)} passes/step, batch {n_local} of "
+        f"{N_global}, {torch.cuda.memory_allocated(dev) / 2**30:.1f} GiB resident")
+
+    comm_stream = torch.cuda.Stream(device=dev) if comm is not None else None
 
     def step(events=None):
-        for idx, (s, li, name, pp, _) in enumerate(work):
+        for idx, (tag, li, name, pp, _, dgb) in enumerate(work):
             if events is not None:
                 events[idx][0].record(stream)
             pp.launch(sptr)
             if events is not None:
                 events[idx][1].record(stream)
-            if distributed and name == "bww":
-                # BWW weight-gradient exchange: NCCL allreduce (sum) over NVLink,
-                # on a comm stream so it overlaps the next layer's passes
+            if comm is not None and name == "bww":
+                # BWW weight-gradient exchange: in-place NCCL allreduce (sum) of
+                # this layer's dG (symmetric window) on a comm stream, so it
+                # overlaps the next layer's passes
                 ev = torch.cuda.Event()
                 ev.record(stream)
                 comm_stream.wait_event(ev)
-                with torch.cuda.stream(comm_stream):
-                    dist.all_reduce(pp.out)
-        if distributed:
+                comm.allreduce(dgb, comm_stream.cuda_stream)
+        if comm is not None:
             stream.wait_stream(comm_stream)
 
     # warmup (also validates every pass once, counters read back)
@@ -296,8 +408,8 @@ def main():
         step()
     torch.cuda.synchronize()
     exec_fmas = {}
-    for (s, li, name, pp, _) in work:
-        exec_fmas[(s, li, name)] = pp.read_counters().executed_vector_fmas
+    for (tag, li, name, pp, _, _) in work:
+        exec_fmas[(tag, li, name)] = pp.read_counters().executed_vector_fmas
     # FFMA peak probe (roofline denominator for the FP32 CUDA-core pipe)
     peak = ffma_peak(sp, dev, sptr)
 
@@ -329,21 +441,21 @@ def main():
         total_ms = float(t.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    flops_step = sum(w[4] for w in work)
-    value = ws * flops_step / (ms_per_step * 1e-3) / 1e9
+    flops_step = sum(w[4] for w in work)  # global batch: every rank's shard
+    value = flops_step / (ms_per_step * 1e-3) / 1e9
 
-    # per (sparsity, pass) breakdown from the last timed step
+    # per (sparsity, pass) breakdown from the last timed step (this rank)
     sweep = {}
-    for idx, (s, li, name, pp, fl) in enumerate(work):
-        d = sweep.setdefault(f"{s:.1f}", {}).setdefault(name, {"ms": 0.0, "dense_flops": 0.0, "useful_flops": 0.0})
+    for idx, (tag, li, name, pp, fl, _) in enumerate(work):
+        d = sweep.setdefault(tag, {}).setdefault(name, {"ms": 0.0, "dense_flops": 0.0, "useful_flops": 0.0})
         d["ms"] += per_launch_ms[idx]
-        d["dense_flops"] += fl
-        d["useful_flops"] += 2.0 * V * exec_fmas[(s, li, name)]
+        d["dense_flops"] += fl * n_local / N_global
+        d["useful_flops"] += 2.0 * V * exec_fmas[(tag, li, name)]
     breakdown = {}
-    for s, passes in sweep.items():
-        breakdown[s] = {n: {"dense_equiv_gflops": round(v["dense_flops"] / v["ms"] / 1e6, 1),
-                            "useful_gflops": round(v["useful_flops"] / v["ms"] / 1e6, 1),
-                            "ms": round(v["ms"], 3)} for n, v in passes.items()}
+    for tag, passes in sweep.items():
+        breakdown[tag] = {n: {"dense_equiv_gflops": round(v["dense_flops"] / v["ms"] / 1e6, 1),
+                              "useful_gflops": round(v["useful_flops"] / v["ms"] / 1e6, 1),
+                              "ms": round(v["ms"], 3)} for n, v in passes.items()}
 
     # roofline for the dominant kernel family (largest share of the step)
     fam_ms = {n: sum(per_launch_ms[i] for i, w in enumerate(work) if w[2] == n) for n in PASSES}
@@ -364,31 +476,116 @@ def main():
                          "CUDA-event launch duration; peak = live FFMA-pipe probe (MEASURED_PEAKS.json has no "
                          "FP32 entry)",
                 "share_of_step": round(dom_ms / (ms_per_step), 3),
-                "dense_equiv_tflops": round(sum(work[i][4] for i in dom_idx) / (dom_ms * 1e-3) / 1e12, 3)}
+                "dense_equiv_tflops": round(sum(work[i][4] * n_local / N_global for i in dom_idx)
+                                            / (dom_ms * 1e-3) / 1e12, 3)}
 
     # speedup vs the same kernels run dense (zero check off) at sparsity 0
-    dense0 = dense_baseline(sp, wl, layers, dev, sptr, V)
+    dense0 = dense_baseline(sp, wl, args.config, n_local, dev, sptr, V)
     # the optional 3xTF32 tensor-core variant on the same resident work
     tc = None if args.no_tc else tf32x3_variant(args, sp, work, step, stream, ws, distributed)
 
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(args, ws), "gpu_launches": int(launches),
         "clocks": clocks.summary(), "roofline": roofline, "sweep": breakdown,
         "dense_mode_at_s0": dense0,
     }
+    if comm is not None:
+        out["collective"] = {"impl": "spc_bww_allreduce (csrc/comm.cu) on a comm stream",
+                             "nccl_version": sp._lib.load().spc_nccl_version(), "ranks": comm.size,
+                             "dG_symmetric_window": symmetric, "dG_bytes_per_step": 4 * dg_total}
     if tc is not None:
         out["tf32x3_variant"] = tc
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(args, layers)
     if not args.no_e2e:
-        out["e2e"] = e2e(args, sp, work, ws, rank, distributed)
+        out["e2e"] = e2e(args, sp, work, ws, rank, comm)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0 and ws == 1 and not args.no_extra and args.config == "vgg16_b32":
+        del work
+        torch.cuda.empty_cache()
+        out["other_configs"] = other_configs(args)
     if rank == 0:
         emit(out)
+    if comm is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.close()
+    if distributed:
+        dist.destroy_process_group()
+
+
+def other_configs(args):
+    """Driver-run numbers for the other BASELINE configs: each runs as its own
+    bench process (`--config X --no-extra --no-cpu --no-e2e --no-tc`), short."""
+    res = {}
+    for cfg in ("cfg1_single3x3_b16", "resnet34_b64", "resnet50_b64", "fixup_resnet50_b256"):
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", cfg, "--steps", "5", "--warmup", "3",
+               "--no-extra", "--no-cpu", "--no-e2e", "--no-tc"]
+        t0 = time.time()
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+            line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+            d = json.loads(line[-1]) if line else {"error": r.stderr[-500:]}
+        except Exception as e:  # keep the headline line even if one config fails
+            d = {"error": repr(e)}
+        keep = ("value", "unit", "ms_per_step", "config", "dense_mode_at_s0", "sweep", "roofline",
+                "activation_sparsity_mean", "gradient_sparsity_mean", "error")
+        res[cfg] = {k: d[k] for k in keep if k in d}
+        res[cfg]["wall_s"] = round(time.time() - t0, 1)
+    return res
+
+
+def run_chain_bench(args, sp, dev, stream, ws, rank, local, comm, distributed):
+    """BASELINE cfg 5: the Fixup ResNet-50 training step (chain.py) -- FWD,
+    BWI, BWW of all 52 convs with fused epilogues -- on this rank's shard of
+    the global batch of 256, per-block dG allreduce through the product's
+    communicator.  Same weights on every rank (one seed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1911_10175_b200 import chain as CH
+    from paper_1911_10175_b200.dist import CommAllreduce
+    ar = CommAllreduce(comm, dev) if comm is not None else None
+    t0 = time.time()
+    ch = CH.fixup_resnet50(256, world=ws, rank=rank, allreduce=ar)
+    torch.cuda.synchronize()
+    setup = time.time() - t0
+    for _ in range(args.warmup):
+        ch.step(stream)
+    torch.cuda.synchronize()
     if distributed:
         dist.barrier()
+    launches0 = sp.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ch.step(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if distributed:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    flops = ch.global_dense_flops()
+    rep = ch.sparsity_report()
+    out = {"metric": METRIC, "value": round(flops / (ms_step * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded He weights, calibrated Fixup biases, ReLU(N(-t,1)) input)",
+           "config": config_dict(args, ws), "gpu_launches": int((sp.launch_count() - launches0)),
+           "activation_sparsity_mean": round(rep["activation_sparsity_mean"], 4),
+           "gradient_sparsity_mean": round(rep["gradient_sparsity_mean"], 4),
+           "passes_per_step": len(ch.passes), "setup_s": round(setup, 1)}
+    if rank == 0:
+        emit(out)
+    if comm is not None:
+        dist.barrier()
+        comm.close()
+    if distributed:
         dist.destroy_process_group()
 
 
@@ -425,11 +622,11 @@ def tf32x3_variant(args, sp, work, step, stream, ws, distributed):
     per = np.array([a.elapsed_time(b) for a, b in events])
     flops_step = sum(w[4] for w in work)
     sweep = {}
-    for idx, (s, li, name, pp, fl) in enumerate(work):
-        d = sweep.setdefault(f"{s:.1f}", {}).setdefault(name, [0.0, 0.0])
-        d[0] += fl
+    for idx, (tag, li, name, pp, fl, _) in enumerate(work):
+        d = sweep.setdefault(tag, {}).setdefault(name, [0.0, 0.0])
+        d[0] += fl / ws
         d[1] += per[idx]
-    fam = {n: [sum(w[4] for w in work if w[2] == n), sum(per[i] for i, w in enumerate(work) if w[2] == n)]
+    fam = {n: [sum(w[4] / ws for w in work if w[2] == n), sum(per[i] for i, w in enumerate(work) if w[2] == n)]
            for n in PASSES}
     dom = max(fam, key=lambda n: fam[n][1])
     try:
@@ -443,7 +640,7 @@ def tf32x3_variant(args, sp, work, step, stream, ws, distributed):
                 "registers every 8 pipeline stages; spc_set_math(SPC_MATH_TF32X3)",
         "tolerance": "max|got-ref|/max|ref| <= 1e-5 vs the 64-bit oracle (tests/test_gpu_tc.py); measured "
                      "0.5e-6 - 1.4e-6 (the reference CPU fp32 kernels: 0.4e-6 - 1.0e-6)",
-        "value": round(ws * flops_step / (ms_step * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+        "value": round(flops_step / (ms_step * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
         "ms_per_step": round(ms_step, 3),
         "sweep": {s: {n: {"dense_equiv_gflops": round(f / ms / 1e6, 1), "ms": round(ms, 3)}
                       for n, (f, ms) in d.items()} for s, d in sweep.items()},
@@ -483,14 +680,15 @@ def load_traffic(family):
         return None, None
 
 
-def dense_baseline(sp, wl, layers, dev, sptr, V):
+def dense_baseline(sp, wl, config, n_local, dev, sptr, V):
     """Same kernels, run_mode::dense (zero check off), at sparsity 0 -- the
-    speedup denominator (P/src/bench.cpp:227-236).  One pass of each layer."""
+    speedup denominator (P/src/bench.cpp:227-236).  One pass of each layer
+    of `config` on this rank's batch shard."""
     import torch
     gen = torch.Generator(device=dev).manual_seed(7)
     tot = {n: [0.0, 0.0] for n in PASSES}
-    for layer in layers:
-        sh = layer.shape
+    for spec in wl.SPECS[config]():
+        sh = sp.ConvShape.make(n_local, spec[2], spec[3], spec[4], spec[4], spec[5], spec[5], spec[6], spec[6])
         G = wl.device_weights(sh.K, sh.C, sh.S, sh.R, gen)
         bD = sp.pack_act_nchwc(wl.device_activation((sh.N, sh.C, sh.H, sh.W), 0.0, gen), V)
         bY = sp.pack_act_nchwc(wl.device_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), 0.0, gen), V)
@@ -512,37 +710,58 @@ def dense_baseline(sp, wl, layers, dev, sptr, V):
     return {n: {"dense_equiv_gflops": round(f / ms / 1e6, 1), "ms": round(ms, 3)} for n, (f, ms) in tot.items()}
 
 
-def cpu_baseline(args, layers):
+def cpu_baseline(args):
+    """The reference library on the box's host cores: sparse over the grid and
+    dense mode at s = 0 (its own speedup denominator, P/src/bench.cpp:227-236),
+    one full 16-image lane block per layer."""
     import oracle
     if not oracle.ref_available():
         return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
     workers = os.cpu_count() or 1
-    f, s = reference_sample(layers, args.grid, args.cpu_images, workers)
+    n_img = args.ref_images or ref_images(args.config)
+    grid = ref_grid(args.config, args.grid)
+    f, s = reference_sample(args.config, grid, n_img, workers, seed=1)
+    fd, sd = reference_sample(args.config, [0.0] if grid != [None] else [None], n_img, workers, mode=1, seed=2)
     return {"value": round(f / s / 1e9, 3), "unit": "GFLOP/s", "cores": workers, "kind": "reference",
-            "sample": f"{args.cpu_images} image(s) per layer x {len(layers)} layers of {args.config} x FWD/BWI/BWW x sparsity "
-                      f"{list(args.grid)} ({f / 1e9:.0f} dense-equiv GFLOP in {s:.1f} s); reference "
-                      f"run_parallel, backend automatic, {workers} workers"}
+            "cpu_model": cpu_model(),
+            "dense_mode_at_s0": {"value": round(fd / sd / 1e9, 3), "unit": "GFLOP/s",
+                                 "speedup_of_sparse": round((f / s) / (fd / sd), 3)},
+            "sample": f"{n_img} image(s) per layer x {len(ref_layers(args.config))} layers of {args.config} x "
+                      f"FWD/BWI/BWW x sparsity {grid} ({f / 1e9:.0f} dense-equiv GFLOP in {s:.1f} s); reference "
+                      f"run_parallel, backend automatic, {workers} threads"}
 
 
-def e2e(args, sp, work, ws, rank, distributed=False):
+def e2e(args, sp, work, ws, rank, comm=None):
     """Same metric through the host-buffer C ABI (spc_run_parallel_host):
-    pinned host inputs -> H2D -> kernels -> D2H of every output, per call."""
+    host inputs -> H2D -> kernels -> D2H of every output, per call; under
+    N > 1 each BWW's partial dG is then summed across ranks (H2D, allreduce,
+    D2H: counted in the bytes).  Pinned host buffers (the headline) and, for
+    one step, pageable ones (what a std::vector caller passes)."""
+    import ctypes
+
+    import numpy as np
     import torch
-    host = []
+    host, tags = [], []
     h2d = d2h = 0
-    for (s, li, name, pp, fl) in work:
+    for (tag, li, name, pp, fl, dgb) in work:
         a = sp.BlockedTensor(**{**pp._a.header(), "data": pp._a.data.cpu().pin_memory().numpy()})
         b = sp.BlockedTensor(**{**pp._b.header(), "data": pp._b.data.cpu().pin_memory().numpy()})
         out = torch.empty(pp.out.numel(), dtype=torch.float32).pin_memory().numpy()
-        host.append((a, b, pp, out, fl))
+        host.append((a, b, pp, out, fl, name))
+        tags.append(tag)
         h2d += (a.data.nbytes + b.data.nbytes)
         d2h += out.nbytes + 32
-    import ctypes
+        if comm is not None and name == "bww":
+            h2d += out.nbytes
+            d2h += out.nbytes
     L = sp._lib.load()
+    scratch = None
+    if comm is not None:
+        scratch = torch.empty(max(h[3].size for h in host if h[5] == "bww"), dtype=torch.float32, device="cuda")
 
-    def one_step():
-        for a, b, pp, out, fl in host:
+    def one_step(items):
+        for a, b, pp, out, fl, name in items:
             ca, cb = a.to_c(), b.to_c()
             cd = sp._lib.spc_tensor(0, 0, 0, 0, 0, 0, 0, 0, 0, out.ctypes.data, out.size)
             cnt = sp._lib.spc_counters()
@@ -550,22 +769,50 @@ def e2e(args, sp, work, ws, rank, distributed=False):
                                          ctypes.byref(pp._plan), 0, ctypes.byref(cd), ctypes.byref(cnt))
             if st:
                 raise sp.SpconvError(st, sp._lib.last_error())
+            if comm is not None and name == "bww":
+                d = scratch[:out.size]
+                d.copy_(torch.from_numpy(out), non_blocking=True)
+                comm.allreduce(d, torch.cuda.current_stream().cuda_stream)
+                torch.from_numpy(out).copy_(d)
 
-    one_step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        one_step()
-    secs = (time.perf_counter() - t0) / args.e2e_steps
-    if distributed:
-        import torch.distributed as dist
-        t = torch.tensor([secs], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        secs = float(t.item())
+    def timed(items, steps):
+        one_step(items)
+        torch.cuda.synchronize()
+        if comm is not None:
+            import torch.distributed as dist
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one_step(items)
+        secs = (time.perf_counter() - t0) / steps
+        if comm is not None:
+            import torch.distributed as dist
+            t = torch.tensor([secs], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            secs = float(t.item())
+        return secs
+
     flops = sum(h[4] for h in host)
-    return {"value": round(ws * flops / secs / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "s_per_step": round(secs, 3),
-            "path": "spc_run_parallel_host (include/spconv_b200.h), pinned host buffers, per-call H2D+D2H+sync"}
+    secs = timed(host, args.e2e_steps)
+    res = {"value": round(flops / secs / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "s_per_step": round(secs, 3),
+           "path": "spc_run_parallel_host (include/spconv_b200.h), pinned host buffers, per-call H2D+D2H+sync"
+                   + ("; BWW dG allreduced across ranks" if comm is not None else "")}
+    # pageable host memory (a std::vector caller): the same calls on the first
+    # sparsity's passes (bounded host RAM), one step
+    page = []
+    for (a, b, pp, out, fl, name), tag in zip(host, tags):
+        if tag != tags[0]:
+            continue
+        pa = sp.BlockedTensor(**{**a.header(), "data": np.array(a.data, copy=True)})
+        pb = sp.BlockedTensor(**{**b.header(), "data": np.array(b.data, copy=True)})
+        page.append((pa, pb, pp, np.empty_like(out), fl, name))
+    pflops = sum(h[4] for h in page)
+    del host
+    ps = timed(page, 1)
+    res["pageable"] = {"value": round(pflops / ps / 1e9, 1), "s_per_step": round(ps, 3),
+                       "path": f"same calls with pageable (numpy) host buffers, sparsity {tags[0]} passes only"}
+    return res
 
 
 if __name__ == "__main__":

@@ -18,6 +18,10 @@
  *   spc_backend_name    <- conv_result::backend / backend_names  kernels.hpp:47-54
  *   spc_relu / spc_relu_grad_mask <- relu / relu_grad_mask  P/include/spconv/sparsity.hpp:14-18
  *   spc_gen_sparse      <- spconv::gen_sparse    P/include/spconv/sparsity.hpp (P/src/sparsity.cpp:42-55)
+ *   spc_vector_probes   <- spconv::vector_probes P/include/spconv/kernels.hpp:90-98
+ *   spc_bww_allreduce / spc_bww_sharded / spc_comm_*: no reference counterpart
+ *                       (the reference is single-process, P/src/kernels.cpp:76-102);
+ *                       the batch-sharded BWW exchange of SURVEY.md 8(e)
  *
  * Conventions
  *   - Plain pointers and sizes only; no C++ types or exceptions cross the ABI.
@@ -135,15 +139,18 @@ spc_status spc_run_parallel(const spc_tensor* a, const spc_tensor* b, const spc_
 
 /* ---- fused output epilogue for layer chains ----
  * Applied per output element as the kernel writes it:
- *   v = acc * alpha (+ add[i]);  if (relu) v = v > 0 ? v : 0;  if (mask) v = mask[i] > 0 ? v : 0
+ *   v = acc * alpha (+ add[i]) (+ beta);  if (relu) v = v > 0 ? v : 0;  if (mask) v = mask[i] > 0 ? v : 0
  * i.e. the reference's relu / relu_grad_mask (P/src/sparsity.cpp:11-28) fused
  * into FWD/BWI.  `add` and `mask` are DEVICE buffers with the output's layout
- * and numel (ActNCHWc); NULL disables them.  {1, NULL, NULL, 0} = plain pass. */
+ * and numel (ActNCHWc); NULL disables them.  `beta` is a scalar bias added
+ * after the (fused) residual add (0 = none; Fixup's bias before the ReLU).
+ * {1, NULL, NULL, 0, 0} = plain pass. */
 typedef struct {
     float alpha;
     const float* add;
     const float* mask;
     int relu;
+    float beta;
 } spc_epilogue;
 spc_status spc_sparse_fwd_ex(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
                              const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
@@ -183,6 +190,38 @@ spc_status spc_gen_sparse(float* out, size_t count, double sparsity, uint64_t se
 
 /* ---- device layout conversion: ActNCHWc -> ActCHWNn (tensor.cpp:94-108) ---- */
 spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stream);
+
+/* ---- multi-GPU: batch-sharded passes, BWW weight-gradient exchange ----
+ * One process per GPU.  FWD/BWI run each rank's contiguous ActNCHWc batch slice
+ * with no communication; BWW computes the slice's partial dG and the ranks sum
+ * it (NCCL allreduce, fp32, in place, on the caller's stream, no host sync).
+ * NCCL is loaded at run time (libnccl.so.2); without it these return SPC_ERR_NCCL.
+ * Communicator setup: rank 0 calls spc_comm_unique_id, the host broadcasts
+ * the SPC_COMM_ID_BYTES bytes, every rank calls spc_comm_init on its device. */
+#define SPC_COMM_ID_BYTES 128
+typedef struct spc_comm spc_comm;
+int spc_nccl_version(void); /* NCCL_VERSION_CODE of the loaded library, 0 if none */
+spc_status spc_comm_unique_id(unsigned char* id /* [SPC_COMM_ID_BYTES] */);
+spc_status spc_comm_init(spc_comm** comm, int nranks, const unsigned char* id, int rank);
+/* Wrap an existing ncclComm_t (not destroyed by spc_comm_destroy). */
+spc_status spc_comm_wrap(spc_comm** comm, void* nccl_comm);
+void* spc_comm_nccl(spc_comm* comm); /* the ncclComm_t */
+int spc_comm_size(spc_comm* comm);
+int spc_comm_rank(spc_comm* comm);
+spc_status spc_comm_destroy(spc_comm* comm);
+/* Collective (all ranks, same sizes, same order): a device buffer in
+ * ncclMemAlloc memory registered as an NCCL symmetric window
+ * (NCCL_WIN_COLL_SYMMETRIC) when the library supports it (*symmetric = 1).
+ * BWW dG buffers placed here are reduced by NCCL's symmetric kernels. */
+spc_status spc_comm_window_alloc(spc_comm* comm, size_t bytes, void** ptr, int* symmetric);
+spc_status spc_comm_window_free(spc_comm* comm, void* ptr);
+/* In-place fp32 sum of n floats across the ranks of `nccl_comm` (an ncclComm_t). */
+spc_status spc_bww_allreduce(void* nccl_comm, float* dG, size_t n, void* stream);
+/* spc_sparse_bww over this rank's shard (shard_shape->N = local images), then
+ * the dG allreduce and a u64 sum of d_counters, all on `stream`. */
+spc_status spc_bww_sharded(spc_comm* comm, const spc_tensor* input, const spc_tensor* grad_out,
+                           const spc_shape* shard_shape, const spc_plan* plan, int mode, spc_tensor* dst,
+                           spc_counters* d_counters, void* stream);
 
 /* ---- introspection ---- */
 const char* spc_last_error(void);

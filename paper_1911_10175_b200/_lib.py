@@ -28,7 +28,8 @@ class spc_plan(C.Structure):
 
 
 class spc_epilogue(C.Structure):
-    _fields_ = [("alpha", C.c_float), ("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int)]
+    _fields_ = [("alpha", C.c_float), ("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int),
+                ("beta", C.c_float)]
 
 
 class spc_counters(C.Structure):
@@ -85,6 +86,20 @@ _SIGS = {
     "spc_debug_conv_variant": (C.c_int, [C.c_int, C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
                                          C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p,
                                          C.c_void_p]),
+    # multi-GPU: batch-sharded BWW exchange (csrc/comm.cu)
+    "spc_nccl_version": (C.c_int, []),
+    "spc_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "spc_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_int]),
+    "spc_comm_wrap": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p]),
+    "spc_comm_nccl": (C.c_void_p, [C.c_void_p]),
+    "spc_comm_size": (C.c_int, [C.c_void_p]),
+    "spc_comm_rank": (C.c_int, [C.c_void_p]),
+    "spc_comm_destroy": (C.c_int, [C.c_void_p]),
+    "spc_comm_window_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
+    "spc_comm_window_free": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "spc_bww_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "spc_bww_sharded": (C.c_int, [C.c_void_p, C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
+                                  C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p, C.c_void_p]),
 }
 
 # Every symbol include/spconv_b200.h declares (checked by the CPU test suite).

@@ -431,12 +431,14 @@ def math_mode(m: Math):
 @dataclasses.dataclass
 class Epilogue:
     """Fused FWD/BWI output epilogue (include/spconv_b200.h spc_epilogue):
-    v = acc*alpha (+ add); relu -> v > 0 ? v : 0; mask -> mask > 0 ? v : 0.
-    `add` / `mask` are device tensors with the output's ActNCHWc layout."""
+    v = acc*alpha (+ add) (+ beta); relu -> v > 0 ? v : 0; mask -> mask > 0 ? v : 0.
+    `add` / `mask` are device tensors with the output's ActNCHWc layout;
+    `beta` a scalar bias (Fixup's bias before the ReLU)."""
     alpha: float = 1.0
     add: object = None
     mask: object = None
     relu: bool = False
+    beta: float = 0.0
 
     def to_c(self) -> "_lib.spc_epilogue":
         def ptr(t):
@@ -447,7 +449,8 @@ class Epilogue:
             if not _is_torch_cuda(t):
                 raise SpconvError(_lib.SPC_ERR_ARG, "epilogue tensors must be CUDA tensors")
             return t.data_ptr()
-        return _lib.spc_epilogue(float(self.alpha), ptr(self.add), ptr(self.mask), 1 if self.relu else 0)
+        return _lib.spc_epilogue(float(self.alpha), ptr(self.add), ptr(self.mask), 1 if self.relu else 0,
+                                 float(self.beta))
 
 
 def epilogue_apply(epi: Epilogue, t) -> None:

@@ -21,12 +21,25 @@ forward pass itself and no tensor leaves the GPU:
              dG1 = BWW(x, da);  dGp = BWW(x, dz) [projection]
              dz' = (x > 0) ? BWI1(da) + (dz or BWIp(dz)) : 0    BWI, epilogue add/mask
 
-Fixup details: the scalar biases are 0 (they would erase
-D's zeros; the paper removed them), one scalar multiplier per
-residual branch.  BWW checks the input side (ActCHWNn copies made on device
-per layer, P/src/tensor.cpp:94-108).  Each block's weight gradients are
-summed across ranks (NCCL on a side stream) as soon as its BWW passes are
-enqueued, overlapping the rest of the backward pass.
+Fixup details: one scalar multiplier per residual branch, and a scalar bias
+before each ReLU (fused as the epilogue's `beta`):
+    a = relu(conv1(x) + b1), b = relu(conv2(a) + b2), out = relu(scale*conv3(b) + sc + b3).
+BASELINE cfg 5 asks for "ReLU masks from a seeded forward pass with ~0.7 mean
+activation sparsity"; with He-normal weights and zero biases the pre-
+activations are centred and ReLU zeroes only ~half of them, so the biases
+are CALIBRATED on that seeded forward pass: each is minus the
+`target_sparsity` quantile of its pre-activation over the first
+`calib_images` images of the global batch (rank 0 computes them and, under
+torch.distributed, broadcasts them, so every rank -- and every world size --
+runs the same network).  BWW checks the input side (ActCHWNn copies made on
+device per layer, P/src/tensor.cpp:94-108).  Each block's weight gradients
+are summed across ranks (NCCL on a side stream) as soon as its BWW passes
+are enqueued, overlapping the rest of the backward pass.
+
+Data parallelism: the global batch `N` is generated once from `seed` and
+each rank keeps its contiguous slice (``dist.shard_range``); the weights come
+from the same seed on every rank, so a multi-rank step equals the
+single-rank full-batch step up to the summation order of dG.
 """
 from __future__ import annotations
 
@@ -113,10 +126,16 @@ class FixupChain:
     FilterKCRSblk (K, C) slice per conv, in ``convs`` order)."""
 
     def __init__(self, N: int, blocks: list[Bottleneck], scale: float = 0.25, seed: int = 0, V: int = 16,
-                 device="cuda", mode: RunMode = RunMode.sparse, allreduce=None, x_sparsity: float = 0.7):
+                 device="cuda", mode: RunMode = RunMode.sparse, allreduce=None, x_sparsity: float = 0.7,
+                 target_sparsity: float | None = 0.7, calib_images: int = 8, world: int = 1, rank: int = 0,
+                 bias: dict | None = None):
         import torch
         from . import workloads as wl
+        from .dist import shard_range
         self.torch = torch
+        self.N_global = N
+        self.shard = shard_range(N, world, rank)
+        N = self.shard[1]
         self.N, self.blocks, self.scale, self.V, self.mode = N, blocks, scale, V, mode
         self.allreduce = allreduce
         g = torch.Generator(device=device).manual_seed(seed)
@@ -161,19 +180,24 @@ class FixupChain:
             self.grad_slice[name] = self.grads[off:off + n]
             off += n
 
-        # ---- activations: network input x0 = ReLU(N(-t,1)) at x_sparsity
+        # ---- activations: network input x0 = ReLU(N(-t,1)) at x_sparsity, the
+        # whole global batch from the seed, this rank's slice kept
         b0 = blocks[0]
-        x0 = wl.device_activation((N, b0.cin, b0.H, b0.W), x_sparsity, g)
+        x0 = wl.device_activation((self.N_global, b0.cin, b0.H, b0.W), x_sparsity, g)
+        x0 = x0[self.shard[0]:self.shard[0] + N].contiguous()
         from .api import pack_act_nchwc
         self.x0 = pack_act_nchwc(x0, V)
+        del x0
         x = self.x0
         self.acts = []  # per block: dict of BlockedTensors
+        self._relu_passes = []  # (conv name, FWD pass with a ReLU epilogue) in forward order
         max_chwnn = 0
         for bi, (b, (s1, s2, s3, sp_)) in enumerate(zip(blocks, specs)):
             G1, G2, G3 = self.weights[f"b{bi}.c1"], self.weights[f"b{bi}.c2"], self.weights[f"b{bi}.c3"]
             p1 = PreparedPass(x, G1[0], s1, plan(s1, Component.fwd, V), mode, epilogue=Epilogue(relu=True))
             a = p1.desc
             p2 = PreparedPass(a, G2[0], s2, plan(s2, Component.fwd, V), mode, epilogue=Epilogue(relu=True))
+            self._relu_passes += [(f"b{bi}.c1", p1), (f"b{bi}.c2", p2)]
             bt = p2.desc
             launch = [p1, p2]
             if sp_ is not None:
@@ -188,6 +212,7 @@ class FixupChain:
                               epilogue=Epilogue(alpha=scale, add=sc.data, relu=True))
             out = p3.desc
             launch.append(p3)
+            self._relu_passes.append((f"b{bi}.c3", p3))
             self._fwd += launch
             for nm, sh in (("c1", s1), ("c2", s2), ("c3", s3)):
                 self.passes.append((f"b{bi}.{nm}", Component.fwd, sh))
@@ -196,6 +221,13 @@ class FixupChain:
                 max_chwnn = max(max_chwnn, ((t.n + V - 1) // V) * t.c * t.h * t.w * V)
             x = out
         self.out = x
+        self.bias = {name: 0.0 for name, _ in self._relu_passes}
+        if bias is not None:  # given (e.g. another rank's calibration)
+            for name, p in self._relu_passes:
+                self.bias[name] = float(bias[name])
+                p._epi.beta = self.bias[name]
+        elif target_sparsity is not None:
+            self._calibrate(target_sparsity, calib_images, device)
 
         # ---- backward
         self.chwnn = torch.empty(max_chwnn, dtype=torch.float32, device=device)
@@ -255,13 +287,61 @@ class FixupChain:
         self.dx0 = dz
 
     # ------------------------------------------------------------------
+    def _calibrate(self, target: float, calib_images: int, device) -> None:
+        """Fixup biases from a seeded forward pass: run the forward with each
+        ReLU pass's epilogue switched to identity, take the `target` quantile
+        tau of its pre-activation over the first `calib_images` images of
+        the global batch (rank 0's slice), set beta = -tau, apply the ReLU
+        (so the next layer sees the calibrated activation), continue.  Rank 0's
+        values are broadcast when torch.distributed is initialised."""
+        torch = self.torch
+        st = torch.cuda.current_stream()
+        relu_of = {id(p): name for name, p in self._relu_passes}
+        ncal = max(1, min(calib_images, self.N))
+        for p in self._fwd:
+            name = relu_of.get(id(p))
+            if name is None:
+                p.launch(st.cuda_stream)
+                continue
+            p._epi.relu = 0
+            p._epi.beta = 0.0
+            p.launch(st.cuda_stream)
+            z = p.out[: p.out.numel() // self.N * ncal]
+            idx = torch.randint(0, z.numel(), (min(z.numel(), 1 << 22),), device=z.device,
+                                generator=torch.Generator(device=z.device).manual_seed(17))
+            tau = float(torch.quantile(z[idx].double(), target))
+            beta = self._bcast(-tau)
+            self.bias[name] = beta
+            p._epi.relu = 1
+            p._epi.beta = beta
+            # the calibrated activation for the layers that follow (setup only)
+            v = p.out + beta
+            p.out.copy_(torch.where(v > 0, v, torch.zeros((), device=v.device)))
+        torch.cuda.synchronize()
+
+    def _bcast(self, v: float) -> float:
+        torch = self.torch
+        import torch.distributed as dist
+        v = float(self.torch.tensor(v, dtype=torch.float32))  # the float32 the epilogue applies
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            t = torch.tensor([v], dtype=torch.float32, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.broadcast(t, src=0)
+            v = float(t.item())
+        return v
+
+    def global_dense_flops(self) -> int:
+        """Dense-equivalent FLOPs of one step over the GLOBAL batch (all ranks)."""
+        return sum(sh.with_batch(self.N_global).dense_flops() for _, _, sh in self.passes)
+
     def set_upstream(self, dout_plain=None, sparsity: float = 0.0):
-        """Upstream gradient w.r.t. the last block output (N(0,1) by default)."""
+        """Upstream gradient w.r.t. the last block output: N(0,1) over the
+        global batch from the chain's generator, this rank's slice (default)."""
         torch = self.torch
         from .api import pack_act_nchwc
         last = self.acts[-1]["out"]
         if dout_plain is None:
-            dout_plain = torch.randn((last.n, last.c, last.h, last.w), device=self.dout.device, generator=self.gen)
+            full = torch.randn((self.N_global, last.c, last.h, last.w), device=self.dout.device, generator=self.gen)
+            dout_plain = full[self.shard[0]:self.shard[0] + last.n]
         self.dout.copy_(pack_act_nchwc(dout_plain, self.V).data)
 
     def forward(self, stream_ptr: int) -> None:
@@ -322,8 +402,11 @@ class _MaskedCopy:
 
 
 def fixup_resnet50(N: int, **kw) -> FixupChain:
-    """BASELINE cfg 5 at batch N (224x224 input, so 56x56 into stage 1)."""
-    return FixupChain(N, resnet50_blocks(), **kw)
+    """BASELINE cfg 5 at global batch N (224x224 input, so 56x56 into stage 1);
+    `world`/`rank` select this rank's batch shard."""
+    ch = FixupChain(N, resnet50_blocks(), **kw)
+    ch.set_upstream()
+    return ch
 
 
 __all__ = ["Bottleneck", "resnet50_blocks", "FixupChain", "fixup_resnet50", "math"]

@@ -33,6 +33,8 @@ static spc_status fail(spc_status st, const std::string& msg) {
     g_err = msg;
     return st;
 }
+// For the other translation units (comm.cu): same thread-local message.
+spc_status set_error(spc_status st, const std::string& msg) { return fail(st, msg); }
 
 static bool valid_V(int v) { return v == 4 || v == 8 || v == 16; }
 static int out_w(const spc_shape& s) { return (s.W + 2 * s.padW - s.R) / s.O + 1; }
@@ -325,6 +327,7 @@ static Epi to_epi(const spc_epilogue* e) {
         d.add = e->add;
         d.mask = e->mask;
         d.relu = e->relu;
+        d.beta = e->beta;
     }
     return d;
 }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/spconv_b200.h"
 
 namespace spc {
@@ -14,18 +16,21 @@ struct DevShape {
     int Hp, Wp;  // out_h(), out_w()  (P/include/spconv/tensor.hpp:44-45)
 };
 
-// Fused output epilogue of FWD/BWI: out = acc*alpha (+ add),
-// then ReLU (v > 0 ? v : 0, P/src/sparsity.cpp:13), then the ReLU-gradient
-// mask (mask > 0 ? v : 0, P/src/sparsity.cpp:26).  `add` and `mask` have
-// the output's ActNCHWc layout.  The identity epilogue leaves acc untouched.
+// Fused output epilogue of FWD/BWI: out = acc*alpha (+ add)
+// (+ beta, a scalar bias: Fixup's), then ReLU (v > 0 ? v : 0,
+// P/src/sparsity.cpp:13), then the ReLU-gradient mask (mask > 0 ? v : 0,
+// P/src/sparsity.cpp:26).  `add` and `mask` have the output's ActNCHWc
+// layout.  The identity epilogue leaves acc untouched.
 struct Epi {
     float alpha = 1.0f;
     const float* add = nullptr;
     const float* mask = nullptr;
     int relu = 0;
-    __host__ __device__ bool active() const { return alpha != 1.0f || add || mask || relu; }
+    float beta = 0.0f;
+    __host__ __device__ bool active() const { return alpha != 1.0f || add || mask || relu || beta != 0.0f; }
     __device__ __forceinline__ float apply(float v, size_t i) const {
         v = add ? fmaf(v, alpha, add[i]) : v * alpha;
+        if (beta != 0.0f) v += beta;
         if (relu) v = v > 0.0f ? v : 0.0f;
         if (mask) v = mask[i] > 0.0f ? v : 0.0f;
         return v;
@@ -152,4 +157,17 @@ __device__ __forceinline__ void fma_lane(float (&a)[KK], float d, const float (&
 // Host-side launch bookkeeping shared by every translation unit.
 namespace spc {
 void note_launch(unsigned n = 1);
+
+// Kernel attributes (cudaFuncSetAttribute) live in the device context, so a
+// "set once" guard must be per device: a process driving several GPUs sets
+// them on each.  Usage: `static PerDeviceOnce g; int d; if (g.needed(d)) {
+// ...set...; g.done(d); }`.
+struct PerDeviceOnce {
+    std::atomic<unsigned long long> mask{0};
+    bool needed(int& dev) {
+        if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+        return ((mask.load(std::memory_order_acquire) >> (dev & 63)) & 1ull) == 0;
+    }
+    void done(int dev) { mask.fetch_or(1ull << (dev & 63), std::memory_order_release); }
+};
 }

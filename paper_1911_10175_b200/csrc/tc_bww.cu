@@ -475,12 +475,13 @@ cudaError_t launch_bww_bn(const CUtensorMap& ahi, const CUtensorMap& alo, const 
     constexpr size_t STAGE = (size_t)PX * (2 * TC_BM * 64 + 2 * BN * 64);
     constexpr int ST = PX == 1 ? TC_ST : (int)((200 * 1024) / STAGE);
     const size_t smem = ST * STAGE + 1024 + 256;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    int attr_dev = 0;
+    if (attr.needed(attr_dev)) {
         cudaError_t e = cudaFuncSetAttribute(tc_bww_kernel<BN, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr.done(attr_dev);
     }
     dim3 grid((unsigned)(g.tgroups * g.ktiles * g.ctiles), (unsigned)g.splits);
     tc_bww_kernel<BN, PX><<<grid, TC_THREADS, smem, st>>>(ahi, alo, bhi, blo, g, partial, nonfinite, cnt, exec_ctr);
@@ -599,14 +600,15 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
         constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * 128 * 64;
         constexpr int PST = 6;
         const size_t smem = PST * STAGE + 1024 + 256;
-        static bool attr = false;
-        if (!attr) {
+        static PerDeviceOnce attr;
+    int attr_dev = 0;
+        if (attr.needed(attr_dev)) {
             e = cudaFuncSetAttribute(tc_bww_pair_kernel<PST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) {
                 cudaFreeAsync(scratch, st);
                 return e;
             }
-            attr = true;
+            attr.done(attr_dev);
         }
         dim3 grid((unsigned)(g.tgroups * g.ktiles * g.ctiles), (unsigned)g.splits);
         tc_bww_pair_kernel<PST><<<grid, TC_THREADS, smem, st>>>(ahi, alo, bhi2, blo2, g, part, nonfinite, cnt, ex);

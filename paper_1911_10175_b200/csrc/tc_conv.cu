@@ -447,13 +447,14 @@ cudaError_t launch_bn(const CUtensorMap& mhi, const CUtensorMap& mlo, const CUte
     // 2-block stages: as many stages as fit 200 KB
     constexpr int ST = KB == 1 ? 4 : (int)((200 * 1024) / STAGE);
     const size_t smem = ST * STAGE + 1024 + 256;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    int attr_dev = 0;
+    if (attr.needed(attr_dev)) {
         cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB, INK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tc_conv_kernel<BN, ST, KB, INK>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr.done(attr_dev);
     }
     TcGeo gg = g;
     gg.N = N;
@@ -723,12 +724,13 @@ cudaError_t launch_pair(const CUtensorMap& mhi, const CUtensorMap& mlo, const CU
     constexpr size_t STAGE = 2 * TC_BM * 64 + 2 * (BN / 2) * 64;
     constexpr int ST = (int)((200 * 1024) / STAGE) > 8 ? 8 : (int)((200 * 1024) / STAGE);
     const size_t smem = ST * STAGE + 1024 + 256;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    int attr_dev = 0;
+    if (attr.needed(attr_dev)) {
         cudaError_t e = cudaFuncSetAttribute(tc_pair_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr.done(attr_dev);
     }
     TcGeo gg = g;
     gg.N = N;
@@ -967,11 +969,12 @@ cudaError_t launch_halo9(const CUtensorMap& mhi, const CUtensorMap& mlo, const C
     constexpr size_t A_HALF = (((size_t)(RW + 2) * P + 8) * 64 + 1023) & ~(size_t)1023;
     constexpr size_t STAGE = 2 * A_HALF + 2 * 9 * 64 * 64;
     const size_t smem = 2 * STAGE + 1024 + 256;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    int attr_dev = 0;
+    if (attr.needed(attr_dev)) {
         cudaError_t e = cudaFuncSetAttribute(tc_halo9_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr.done(attr_dev);
     }
     int ctas = 148;
     if (ctas > g.ntiles) ctas = g.ntiles;

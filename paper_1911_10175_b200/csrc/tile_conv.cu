@@ -568,10 +568,11 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
         kern = sparse ? tile_conv_entry<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, JT, true, false>()
                       : tile_conv_entry<FWD, KK, TH, TW, NWY, NWX, R, S, STR, GPF, 0, false, false>();
     }
-    static bool attr_set[2][2] = {{false, false}, {false, false}};  // per instantiation: [epi][sparse]
-    if (!attr_set[with_epi][sparse]) {
+    static PerDeviceOnce attr_set[2][2];  // per instantiation: [epi][sparse], per device
+    int attr_dev = 0;
+    if (attr_set[with_epi][sparse].needed(attr_dev)) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
-        attr_set[with_epi][sparse] = true;
+        attr_set[with_epi][sparse].done(attr_dev);
     }
     const int Ci = FWD ? sh.C : sh.K;
     const int Hs = FWD ? sh.H : sh.Hp, Ws = FWD ? sh.W : sh.Wp;
@@ -752,7 +753,7 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
         // resolution; KK=4 branches for sparse, the KK=4 4x8 one-warp jump table for
         // density <= 28% (measured crossover near s = 0.7 for the capped one-warp
         // jump table: s = 0.75 3-9% ahead, s = 0.7 even), KK=2 7x7 for dense mode.
-        if (sparse && kk4) {
+        if (sparse && kk4 && xsel == nullptr) {
             const int Ci = fwd ? sh.C : sh.K;
             const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
             int* sel = nullptr;

@@ -53,9 +53,9 @@ def main():
     _, n_local = shard_range(a.batch, ws, rank)
     t0 = time.time()
     ar = GradAllreduce(device=dev) if distributed else None
-    ch = CH.fixup_resnet50(n_local, scale=a.scale, seed=1234 + rank, mode=sp.RunMode[a.mode], allreduce=ar,
-                           x_sparsity=a.x_sparsity)
-    ch.set_upstream()
+    # one seed on every rank: the same weights, each rank its slice of the global batch
+    ch = CH.fixup_resnet50(a.batch, scale=a.scale, seed=1234, mode=sp.RunMode[a.mode], allreduce=ar,
+                           x_sparsity=a.x_sparsity, world=ws, rank=rank)
     st = torch.cuda.current_stream()
     torch.cuda.synchronize()
     setup_s = time.time() - t0
@@ -77,11 +77,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / a.steps
-    flops_local = ch.dense_flops()
-    fl = torch.tensor([float(flops_local)], device=dev, dtype=torch.float64)
-    if distributed:
-        dist.all_reduce(fl)
-    total_flops = float(fl.item())
+    total_flops = float(ch.global_dense_flops())
     rep = ch.sparsity_report()
     out = {"metric": "dense-equiv GFLOP/s per training step (FWD+BWI+BWW, all convs)",
            "value": round(total_flops / (ms_step * 1e-3) / 1e9, 1), "unit": "GFLOP/s", "n_gpus": ws,
@@ -89,7 +85,8 @@ def main():
            "scaling": "strong", "dtype": "f32", "data": "synthetic (seeded He weights, ReLU(N(-t,1)) input)",
            "config": {"workload": "fixup_resnet50: 16 bottlenecks, 52 convs x FWD/BWI/BWW, 224x224",
                       "global_batch": a.batch, "per_gpu_batch": n_local, "mode": a.mode,
-                      "fixup": f"bias = 0, branch multiplier {a.scale}, residual add, ReLU (fused epilogues)",
+                      "fixup": f"calibrated scalar biases (0.7 target), branch multiplier {a.scale}, residual add, "
+                               "ReLU (fused epilogues)",
                       "bww_check": "input", "parallelism": f"dp{ws} (batch-sharded, per-block dG allreduce)"},
            "gpu_launches": int((sp.launch_count() - launches0) / a.steps),
            "activation_sparsity_mean": round(rep["activation_sparsity_mean"], 4),
