@@ -94,8 +94,38 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
         cudaFreeAsync(finite, st);
         return e;
     }
-    if (!force_generic && tile_bww_supported(check_input, sh, V))
-        return launch_tile_bww(check_input, sparse, sh, chk, oth, dst, exec_ctr, st);
+    // V=16 tile kernels (tile_bww.cu).  SPC_ROW_BWW=1 selects the row-window
+    // kernel for 3x3 s1 check=input instead (row_bww.cu: measured 8-30%
+    // slower than the tile kernel on the VGG layers except conv1_2, kept for
+    // A/B).  Both add d * 0 for taps whose partner pixel lies
+    // outside the image (zero-filled staging), exact only for a FINITE checked
+    // tensor: a device scan of it picks, for Inf/NaN, the shape-general
+    // kernel (exact skips, P/src/kernel_impl.hpp:239-304).  All are enqueued;
+    // the non-matching ones exit at entry (no host sync).
+    static const bool row_on = std::getenv("SPC_ROW_BWW") && std::atoi(std::getenv("SPC_ROW_BWW")) == 1;
+    const bool use_row = !force_generic && row_on && row_bww_supported(check_input, sh, V);
+    if (use_row || (!force_generic && tile_bww_supported(check_input, sh, V))) {
+        const size_t chk_n = (size_t)((sh.N + 15) / 16) * 16 *
+                             (check_input ? (size_t)sh.C * sh.H * sh.W : (size_t)sh.K * sh.Hp * sh.Wp);
+        int* finite = nullptr;
+        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        launch_finite_all(chk, chk_n, finite, st);
+        e = use_row ? launch_row_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, st)
+                    : launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, finite, 1);
+        if (e == cudaSuccess) {
+            const int gs = bww_generic_splits(sh);
+            const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
+            float* partial = nullptr;
+            e = cudaMallocAsync((void**)&partial, (size_t)gs * E * sizeof(float), st);
+            if (e == cudaSuccess) {
+                e = launch_bww_generic(check_input, sparse, sh, V, chk, oth, partial, gs, dst, exec_ctr, st, finite, 0);
+                cudaFreeAsync(partial, st);
+            }
+        }
+        cudaFreeAsync(finite, st);
+        return e;
+    }
     const int splits = bww_generic_splits(sh);
     const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
     float* partial = nullptr;

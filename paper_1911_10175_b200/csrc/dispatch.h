@@ -31,6 +31,7 @@ cudaError_t launch_conv_generic(bool fwd, bool sparse, const DevShape& sh, int V
 int bww_generic_splits(const DevShape& sh);
 cudaError_t launch_bww_generic(bool check_input, bool sparse, const DevShape& sh, int V, const float* chk,
                                const float* oth, float* partial, int splits, float* dst,
-                               unsigned long long* exec_ctr, cudaStream_t st);
+                               unsigned long long* exec_ctr, cudaStream_t st, const int* sel = nullptr,
+                               int want = 0);
 
 }  // namespace spc

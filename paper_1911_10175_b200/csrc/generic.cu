@@ -86,7 +86,9 @@ template <bool CheckInput, bool Sparse>
 __global__ void __launch_bounds__(128) bww_generic_partial(DevShape sh, int V, const float* __restrict__ chk,
                                                            const float* __restrict__ oth,
                                                            float* __restrict__ partial, int splits,
-                                                           unsigned long long* __restrict__ exec_ctr) {
+                                                           unsigned long long* __restrict__ exec_ctr,
+                                                           const int* __restrict__ sel, int want) {
+    if (sel != nullptr && __ldg(sel) != want) return;
     const int Lc = CheckInput ? sh.K : sh.C;  // lane channel count
     const int Mc = CheckInput ? sh.C : sh.K;  // checked channel count
     int b = blockIdx.x;
@@ -133,7 +135,8 @@ __global__ void __launch_bounds__(128) bww_generic_partial(DevShape sh, int V, c
 // performs the reference's check=output_grad (c,k) fix-up
 // (P/src/kernels.cpp:285-300) for free: partials are already in (k, c) order.
 __global__ void bww_reduce_kernel(DevShape sh, int V, const float* __restrict__ partial, int splits,
-                                  float* __restrict__ dst) {
+                                  float* __restrict__ dst, const int* __restrict__ sel, int want) {
+    if (sel != nullptr && __ldg(sel) != want) return;
     const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < E; e += (size_t)gridDim.x * blockDim.x) {
         float s = 0.0f;
@@ -178,24 +181,24 @@ int bww_generic_splits(const DevShape& sh) {
 
 cudaError_t launch_bww_generic(bool check_input, bool sparse, const DevShape& sh, int V, const float* chk,
                                const float* oth, float* partial, int splits, float* dst,
-                               unsigned long long* exec_ctr, cudaStream_t st) {
+                               unsigned long long* exec_ctr, cudaStream_t st, const int* sel, int want) {
     const int Lc = check_input ? sh.K : sh.C;
     const int Mc = check_input ? sh.C : sh.K;
     const int bs = Lc >= 128 ? 128 : ((Lc + 31) / 32) * 32;
     dim3 grid((unsigned)(Mc * sh.S * sh.R), (unsigned)((Lc + bs - 1) / bs), (unsigned)splits);
     if (check_input) {
-        if (sparse) bww_generic_partial<true, true><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr);
-        else bww_generic_partial<true, false><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr);
+        if (sparse) bww_generic_partial<true, true><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr, sel, want);
+        else bww_generic_partial<true, false><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr, sel, want);
     } else {
-        if (sparse) bww_generic_partial<false, true><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr);
-        else bww_generic_partial<false, false><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr);
+        if (sparse) bww_generic_partial<false, true><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr, sel, want);
+        else bww_generic_partial<false, false><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr, sel, want);
     }
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
     const unsigned rb = (unsigned)((E + 255) / 256 < 4096 ? (E + 255) / 256 : 4096);
-    bww_reduce_kernel<<<rb, 256, 0, st>>>(sh, V, partial, splits, dst);
+    bww_reduce_kernel<<<rb, 256, 0, st>>>(sh, V, partial, splits, dst, sel, want);
     note_launch();
     return cudaGetLastError();
 }

@@ -12,4 +12,10 @@ cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, 
 cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& sh, const float* chk,
                                  const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st,
                                  const int* sel, int want);
+// row_bww.cu: check = input, 3x3 stride 1 pad 1 (row-streaming window kernel)
+bool row_bww_supported(bool check_input, const DevShape& sh, int V);
+// runs when *sel == 1 (the checked tensor is finite), exits otherwise
+cudaError_t launch_row_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
+                                unsigned long long* exec_ctr, const int* sel, cudaStream_t st);
+
 }  // namespace spc

@@ -575,3 +575,66 @@ def test_pointwise_bww_nonfinite_grad_keeps_skip_semantics(sp, stride):
         fin = np.isfinite(ref_out)
         assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
         assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("K", [64, 128])
+def test_bww_3x3_nonfinite_input_keeps_skip_semantics(sp, K):
+    """The 3x3 BWW tile kernels add d * 0 for output pixels outside the image
+    (tiles overhanging the right/bottom edge: exact only for finite d).  D
+    holding Inf/NaN must switch to the exact-skip kernel: GPU == reference CPU
+    incl. NaN/Inf positions; finite D keeps the tile kernel (same values)."""
+    V = 16
+    sh = sp.ConvShape.make(5, 32, K, 9, 10, 3, 3, 1, 1)
+    rng = np.random.default_rng(K)
+    D = np.maximum(rng.standard_normal((sh.N, sh.C, sh.H, sh.W)) - 0.3, 0).astype(np.float32)
+    dY = rng.standard_normal((sh.N, sh.K, sh.H, sh.W)).astype(np.float32)
+    for finite in (True, False):
+        X = D.copy()
+        if not finite:
+            X[1, 3, 0, 0] = np.inf   # corner pixel: its out-of-image taps must not produce NaN
+            X[2, 7, 4, 9] = np.nan
+        r = O.RefRun(2, 0, sh.astuple(), V, X, dY)
+        r.exec(0, 4)
+        ref_out, ref_cnt, _ = r.result()
+        pl = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck.input)
+        res = sp.run_parallel(sp.pack_act_chwnn(X, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pl,
+                              sp.RunMode.sparse)
+        got = sp.unpack(res.out).cpu().numpy()
+        assert np.array_equal(np.isnan(got), np.isnan(ref_out)), finite
+        assert np.array_equal(np.isinf(got), np.isinf(ref_out)), finite
+        fin = np.isfinite(ref_out)
+        assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
+        assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
+
+
+def test_row_bww_kernel_matches_oracle(tmp_path):
+    """The opt-in row-window BWW kernel (SPC_ROW_BWW=1, csrc/row_bww.cu) on
+    shapes with partial strips, both KK variants, sparse and dense mode,
+    exact counters, and non-finite D (exact fallback)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, oracle as O, paper_1911_10175_b200 as sp
+V = 16
+for (n, C, K, H, W) in [(3, 16, 64, 9, 10), (2, 32, 128, 14, 13), (17, 16, 128, 7, 30), (1, 64, 64, 5, 5)]:
+    sh = sp.ConvShape.make(n, C, K, H, W, 3, 3, 1, 1)
+    for s in (0.0, 0.5, 0.9):
+        D = O.gen_sparse(n, C, H, W, s, n + C)
+        dY = O.gen_sparse(n, K, H, W, 0.0, K + W)
+        ref = O.dense(2, sh.astuple(), D, dY)
+        want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), 2, V), D)
+        pl = sp.plan(sh, sp.Component.bww, V)
+        for mode in (0, 1):
+            res = sp.run_parallel(sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pl,
+                                  sp.RunMode(mode))
+            got = sp.unpack(res.out).cpu().numpy()
+            assert O.max_abs_rel(got, ref) <= 1e-5, (sh, s, mode)
+            assert res.counters.executed_vector_fmas == (want["executed_vector_fmas"] if mode == 0
+                                                         else want["dense_total"]), (sh, s, mode)
+print("ok")
+'''
+    env = dict(os.environ, SPC_ROW_BWW="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]

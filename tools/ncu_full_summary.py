@@ -27,7 +27,12 @@ KEYS = {
 
 
 def summarize(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """`rep`: an .ncu-rep, or the CSV log of `ncu --set full --csv --page raw
+    --log-file X` (the form this pool's ncu wrapper returns intact)."""
+    if rep.endswith(".csv"):
+        raw = "".join(ln for ln in open(rep) if ln.startswith('"'))
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     out = {"report": rep.split("/")[-1], "kernel": vals[hdr.index("Kernel Name")][:160]}
