@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_conv.h"
+#include "dispatch.h"
+#include "pw_bww.h"
 #include "tile_bww.h"
 
 namespace spc {
@@ -411,6 +413,13 @@ __global__ void tc_bww_reduce_kernel(const float* __restrict__ partial, float* _
 // 16-channel block, 16-pixel run) through a shared 16 x 16 x 16 tile: 1 KB
 // contiguous reads (16 px x 16 ch of one image, or 16 px x 16 images of one
 // channel) and 1 KB contiguous writes (16 ch x 16 images of one pixel).
+// Fallback selector of the non-finite path: 0 = the tensor-core result
+// stands, 1 = FFMA tile kernel (checked tensor finite), 2 = generic kernel.
+__global__ void tc_select_kernel(const int* __restrict__ nonfinite, const int* __restrict__ chk_finite,
+                                 int* __restrict__ sel) {
+    *sel = *nonfinite == 0 ? 0 : (*chk_finite ? 1 : 2);
+}
+
 // Flags non-finite values.
 template <bool FROM_CHWNN>
 __global__ void __launch_bounds__(256) tc_to_hwcn_split_kernel(const float* __restrict__ in, float* __restrict__ hi,
@@ -629,8 +638,33 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
         note_launch();
         e = cudaGetLastError();
     }
-    // non-finite operands: the FFMA BWW with the reference's exact skip semantics
-    if (e == cudaSuccess) e = launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, nonfinite, 1);
+    // non-finite operands: the FP32 dispatch with the reference's exact skip
+    // semantics -- the FFMA tile kernel when the checked tensor is finite, the
+    // shape-general kernel otherwise (dispatch.cu launch_bww); sel2 = 0 (TC
+    // ran), 1 (tile), 2 (generic)
+    if (e == cudaSuccess) {
+        int* sel2 = nullptr;
+        e = cudaMallocAsync((void**)&sel2, 2 * sizeof(int), st);
+        if (e == cudaSuccess) {
+            const size_t chk_n = (size_t)((sh.N + 15) / 16) * 16 *
+                                 (check_input ? (size_t)sh.C * sh.H * sh.W : (size_t)sh.K * sh.Hp * sh.Wp);
+            launch_finite_all(chk, chk_n, sel2 + 1, st);
+            tc_select_kernel<<<1, 1, 0, st>>>(nonfinite, sel2 + 1, sel2);
+            note_launch();
+            e = launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, sel2, 1);
+            if (e == cudaSuccess) {
+                const int gs = bww_generic_splits(sh);
+                const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
+                float* gpart = nullptr;
+                e = cudaMallocAsync((void**)&gpart, (size_t)gs * E * sizeof(float), st);
+                if (e == cudaSuccess) {
+                    e = launch_bww_generic(check_input, sparse, sh, 16, chk, oth, gpart, gs, dst, exec_ctr, st, sel2, 2);
+                    cudaFreeAsync(gpart, st);
+                }
+            }
+            cudaFreeAsync(sel2, st);
+        }
+    }
     cudaFreeAsync(scratch, st);
     return e;
 }

@@ -578,34 +578,40 @@ def test_pointwise_bww_nonfinite_grad_keeps_skip_semantics(sp, stride):
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
-@pytest.mark.parametrize("K", [64, 128])
-def test_bww_3x3_nonfinite_input_keeps_skip_semantics(sp, K):
-    """The 3x3 BWW tile kernels add d * 0 for output pixels outside the image
-    (tiles overhanging the right/bottom edge: exact only for finite d).  D
-    holding Inf/NaN must switch to the exact-skip kernel: GPU == reference CPU
-    incl. NaN/Inf positions; finite D keeps the tile kernel (same values)."""
+@pytest.mark.parametrize("K,stride,check", [(64, 1, 0), (128, 1, 0), (128, 2, 0), (64, 1, 1), (128, 2, 1)])
+def test_bww_3x3_nonfinite_checked_keeps_skip_semantics(sp, K, stride, check):
+    """The 3x3 BWW tile kernels add d * 0 for partner pixels outside the image
+    (tiles overhanging the right/bottom edge, virtual padding): exact only for
+    a finite checked tensor.  A checked tensor holding Inf/NaN must switch to
+    the exact-skip kernel: GPU == reference CPU incl. NaN/Inf positions, in
+    both arithmetics; finite tensors keep the tile kernels (same values)."""
     V = 16
-    sh = sp.ConvShape.make(5, 32, K, 9, 10, 3, 3, 1, 1)
-    rng = np.random.default_rng(K)
+    sh = sp.ConvShape.make(5, 32, K, 9, 10, 3, 3, stride, stride)
+    hp, wp = sh.out_h(), sh.out_w()
+    rng = np.random.default_rng(K + 10 * stride + check)
     D = np.maximum(rng.standard_normal((sh.N, sh.C, sh.H, sh.W)) - 0.3, 0).astype(np.float32)
-    dY = rng.standard_normal((sh.N, sh.K, sh.H, sh.W)).astype(np.float32)
+    dY = np.maximum(rng.standard_normal((sh.N, sh.K, hp, wp)) - 0.3, 0).astype(np.float32)
     for finite in (True, False):
-        X = D.copy()
+        X, Y = D.copy(), dY.copy()
         if not finite:
-            X[1, 3, 0, 0] = np.inf   # corner pixel: its out-of-image taps must not produce NaN
-            X[2, 7, 4, 9] = np.nan
-        r = O.RefRun(2, 0, sh.astuple(), V, X, dY)
+            T = X if check == 0 else Y
+            T[1, 3, 0, 0] = np.inf   # corner: its out-of-image partners must not produce NaN
+            T[2, 7, T.shape[2] - 1, T.shape[3] - 1] = np.nan
+        r = O.RefRun(2, check, sh.astuple(), V, X, Y)
         r.exec(0, 4)
         ref_out, ref_cnt, _ = r.result()
-        pl = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck.input)
-        res = sp.run_parallel(sp.pack_act_chwnn(X, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pl,
-                              sp.RunMode.sparse)
-        got = sp.unpack(res.out).cpu().numpy()
-        assert np.array_equal(np.isnan(got), np.isnan(ref_out)), finite
-        assert np.array_equal(np.isinf(got), np.isinf(ref_out)), finite
-        fin = np.isfinite(ref_out)
-        assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
-        assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
+        pl = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck(check))
+        a = sp.pack_act_chwnn(X, V) if check == 0 else sp.pack_act_nchwc(X, V)
+        b = sp.pack_act_nchwc(Y, V) if check == 0 else sp.pack_act_chwnn(Y, V)
+        for math in (sp.Math.fp32, sp.Math.tf32x3):
+            with sp.math_mode(math):
+                res = sp.run_parallel(a.to("cuda"), b.to("cuda"), sh, pl, sp.RunMode.sparse)
+            got = sp.unpack(res.out).cpu().numpy()
+            assert np.array_equal(np.isnan(got), np.isnan(ref_out)), (finite, math)
+            assert np.array_equal(np.isinf(got), np.isinf(ref_out)), (finite, math)
+            fin = np.isfinite(ref_out)
+            assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref_out, 0)) <= TOL
+            assert res.counters.executed_vector_fmas == ref_cnt["executed_vector_fmas"]
 
 
 def test_row_bww_kernel_matches_oracle(tmp_path):
