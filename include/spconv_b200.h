@@ -188,6 +188,16 @@ spc_status spc_relu_grad_mask(const float* pre, const float* upstream, float* ou
  * the same tensor, as the reference's sweep/verify harness (bench.cpp:127-180). */
 spc_status spc_gen_sparse(float* out, size_t count, double sparsity, uint64_t seed);
 
+/* ---- vector_probes (P/include/spconv/kernels.hpp:90-98) ----
+ * The contract operations of this backend, run on the device the way the
+ * kernels run them (one warp; lane j = vector lane j), for the reference's
+ * scalar-vs-SIMD equivalence tests: host arrays of V floats in and out.
+ *   SPC_PROBE_CMP_NEQ_ZERO: *mask = bit j set iff a[j] != 0 (-0 -> 0, NaN -> 1)
+ *   SPC_PROBE_BROADCAST_FMA: out[j] = fmaf(s, b[j], a[j])   (acc = a, w = b)
+ *   SPC_PROBE_ADD:           out[j] = a[j] + b[j] */
+typedef enum { SPC_PROBE_CMP_NEQ_ZERO = 0, SPC_PROBE_BROADCAST_FMA = 1, SPC_PROBE_ADD = 2 } spc_probe_op;
+spc_status spc_vector_probe(int V, int op, const float* a, const float* b, float s, float* out, uint32_t* mask);
+
 /* ---- device layout conversion: ActNCHWc -> ActCHWNn (tensor.cpp:94-108) ---- */
 spc_status spc_nchwc_to_chwnn(const spc_tensor* src, spc_tensor* dst, void* stream);
 
@@ -236,11 +246,6 @@ uint64_t spc_launch_count(void);
  * thread running `iters` x 16 independent FFMAs; out[0] receives a checksum.
  * Returns the kernel's FLOP count in *flops (time it with events). */
 spc_status spc_ffma_peak_kernel(float* out, int blocks, int iters, double* flops, void* stream);
-/* Development: run FWD/BWI with tile-kernel variant `variant` (3x3 stride 1,
- * V=16 only; see launch_tile_conv_variant).  Same validation as spc_sparse_*. */
-spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
-                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters,
-                                  void* stream);
 /* Write `n` floats of scratch (an L2 flush between timed steps). */
 spc_status spc_l2_flush(float* scratch, size_t n, void* stream);
 

@@ -83,9 +83,8 @@ _SIGS = {
     "spc_ffma_peak_kernel": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_void_p]),
     "spc_l2_flush": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_gen_sparse": (C.c_int, [C.c_void_p, C.c_size_t, C.c_double, C.c_uint64]),
-    "spc_debug_conv_variant": (C.c_int, [C.c_int, C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
-                                         C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p,
-                                         C.c_void_p]),
+    "spc_vector_probe": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
+                                   C.POINTER(C.c_uint32)]),
     # multi-GPU: batch-sharded BWW exchange (csrc/comm.cu)
     "spc_nccl_version": (C.c_int, []),
     "spc_comm_unique_id": (C.c_int, [C.c_void_p]),
@@ -105,6 +104,14 @@ _SIGS = {
 # Every symbol include/spconv_b200.h declares (checked by the CPU test suite).
 EXPORTED = tuple(_SIGS)
 
+# include/spconv_b200_dev.h (development entry points)
+_DEV_SIGS = {
+    "spc_debug_conv_variant": (C.c_int, [C.c_int, C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
+                                         C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor), C.c_void_p,
+                                         C.c_void_p]),
+}
+DEV_EXPORTED = tuple(_DEV_SIGS)
+
 _lib = None
 
 
@@ -117,7 +124,7 @@ def load():
                 f"{LIB_PATH} is missing: build the CUDA library first "
                 "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback.")
         L = C.CDLL(LIB_PATH)
-        for name, (res, args) in _SIGS.items():
+        for name, (res, args) in {**_SIGS, **_DEV_SIGS}.items():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

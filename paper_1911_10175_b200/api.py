@@ -394,6 +394,41 @@ def backend_names() -> list[str]:
     return [backend_name()]
 
 
+@dataclasses.dataclass
+class VecProbe:
+    """vec_probe (P/include/spconv/kernels.hpp:90-97): this backend's contract
+    operations, executed on the device as the kernels execute them."""
+    name: str
+    width: int
+    native: bool
+
+    def cmp_neq_zero(self, v) -> int:
+        a = np.ascontiguousarray(v, np.float32)
+        m = C.c_uint32()
+        _check(_lib.load().spc_vector_probe(self.width, 0, a.ctypes.data, None, 0.0, None, C.byref(m)))
+        return int(m.value)
+
+    def broadcast_fma(self, acc, s: float, w):
+        a, b = np.ascontiguousarray(acc, np.float32), np.ascontiguousarray(w, np.float32)
+        out = np.empty(self.width, np.float32)
+        _check(_lib.load().spc_vector_probe(self.width, 1, a.ctypes.data, b.ctypes.data, float(s), out.ctypes.data,
+                                            None))
+        return out
+
+    def add(self, a, b):
+        a, b = np.ascontiguousarray(a, np.float32), np.ascontiguousarray(b, np.float32)
+        out = np.empty(self.width, np.float32)
+        _check(_lib.load().spc_vector_probe(self.width, 2, a.ctypes.data, b.ctypes.data, 0.0, out.ctypes.data, None))
+        return out
+
+
+def vector_probes(V: int) -> list[VecProbe]:
+    """vector_probes(V) (P/include/spconv/kernels.hpp:98): the one device backend."""
+    if V not in (4, 8, 16):
+        raise SpconvError(_lib.SPC_ERR_ARG, "vector_probes: V must be 4, 8 or 16")
+    return [VecProbe(backend_name(), V, True)]
+
+
 def launch_count() -> int:
     return int(_lib.load().spc_launch_count())
 

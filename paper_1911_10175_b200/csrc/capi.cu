@@ -14,6 +14,8 @@
 #include <cstring>
 #include <random>
 #include <mutex>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -33,6 +35,20 @@ static spc_status fail(spc_status st, const std::string& msg) {
     g_err = msg;
     return st;
 }
+int* stream_flags(cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, int*> blocks;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    int*& p = blocks[{dev, st}];
+    if (!p && cudaMalloc((void**)&p, FLAG_COUNT * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+    }
+    return p;
+}
+
 // For the other translation units (comm.cu): same thread-local message.
 spc_status set_error(spc_status st, const std::string& msg) { return fail(st, msg); }
 
@@ -252,10 +268,13 @@ static spc_status check_device() {
     if (major != 10 || minor != 0)
         return fail(SPC_ERR_NO_DEVICE, "this library is built for sm_100a (B200); device is sm_" +
                                            std::to_string(major) + std::to_string(minor));
-    // keep stream-ordered workspace allocations cached between calls
+    // keep up to 1 GiB of stream-ordered workspace (BWW split partials,
+    // tensor-core staging) cached between calls; memory above it returns to
+    // the device at synchronisation points, so co-resident allocators
+    // (e.g. PyTorch's) can use it
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        unsigned long long thr = ~0ULL;
+        unsigned long long thr = 1ull << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     if (dev >= 0 && dev < 64) cached_ok[dev] = 1;
@@ -984,11 +1003,17 @@ spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_
         if ((s = check_device())) return s;
         cudaStream_t st = (cudaStream_t)stream;
         if ((s = start_counters(*shape, *plan, mode, d_counters, st))) return s;
+#ifdef SPC_DEV
         const bool ci = plan->check == SPC_CHECK_INPUT;
         cudaError_t e = launch_tile_bww_variant(variant, ci, mode == SPC_SPARSE, make_dev_shape(*shape),
                                                 ci ? src->data : filt->data, ci ? filt->data : src->data, dst->data,
                                                 exec_slot(d_counters, mode), st);
         return e == cudaSuccess ? SPC_OK : cuda_fail(e, "variant launch");
+#else
+        (void)variant;
+        (void)st;
+        return fail(SPC_ERR_ARG, "BWW tuning variants need the development build (make DEV=1)");
+#endif
     }
     const bool fwd = plan->comp == SPC_FWD;
     spc_status s = fwd ? validate_fwd(src, filt, *shape, *plan) : validate_bwi(src, filt, *shape, *plan);
@@ -1000,6 +1025,43 @@ spc_status spc_debug_conv_variant(int variant, const spc_tensor* src, const spc_
     cudaError_t e = launch_tile_conv_variant(variant, fwd, mode == SPC_SPARSE, make_dev_shape(*shape), src->data,
                                              filt->data, dst->data, exec_slot(d_counters, mode), st);
     return e == cudaSuccess ? SPC_OK : cuda_fail(e, "variant launch");
+}
+
+// vector_probes (P/include/spconv/kernels.hpp:90-98): the backend's contract
+// operations exposed for equivalence tests -- here in the form the kernels
+// use them, one warp, lane j = vector lane j: cmp_neq_zero as
+// __ballot_sync(v != 0.0f), broadcast_fma as fmaf per lane, add per lane.
+__global__ void vector_probe_kernel(int V, int op, const float* __restrict__ a, const float* __restrict__ b, float s,
+                                    float* __restrict__ out, unsigned* __restrict__ mask) {
+    const int l = threadIdx.x;
+    const bool in = l < V;
+    const float x = in ? a[l] : 0.0f;
+    if (op == SPC_PROBE_CMP_NEQ_ZERO) {
+        const unsigned m = __ballot_sync(0xffffffffu, in && x != 0.0f);
+        if (l == 0) *mask = m;
+    } else if (in) {
+        out[l] = op == SPC_PROBE_BROADCAST_FMA ? fmaf(s, b[l], x) : x + b[l];
+    }
+}
+
+spc_status spc_vector_probe(int V, int op, const float* a, const float* b, float s, float* out, uint32_t* mask) {
+    if (!valid_V(V)) return fail(SPC_ERR_ARG, "vector_probe: V must be 4, 8 or 16");
+    if (op < SPC_PROBE_CMP_NEQ_ZERO || op > SPC_PROBE_ADD) return fail(SPC_ERR_ARG, "vector_probe: bad op");
+    if (!a || (op == SPC_PROBE_CMP_NEQ_ZERO ? !mask : (!b || !out))) return fail(SPC_ERR_ARG, "null argument");
+    if (spc_status st = check_device()) return st;
+    float* d = nullptr;
+    cudaError_t e = cudaMalloc((void**)&d, 3 * 16 * sizeof(float) + sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "vector_probe alloc");
+    unsigned* dm = reinterpret_cast<unsigned*>(d + 48);
+    cudaMemcpy(d, a, V * sizeof(float), cudaMemcpyHostToDevice);
+    if (b) cudaMemcpy(d + 16, b, V * sizeof(float), cudaMemcpyHostToDevice);
+    vector_probe_kernel<<<1, 32>>>(V, op, d, d + 16, s, d + 32, dm);
+    note_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess && op == SPC_PROBE_CMP_NEQ_ZERO) e = cudaMemcpy(mask, dm, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    else if (e == cudaSuccess) e = cudaMemcpy(out, d + 32, V * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? SPC_OK : cuda_fail(e, "vector_probe");
 }
 
 spc_status spc_gen_sparse(float* out, size_t count, double sparsity, uint64_t seed) {

@@ -158,6 +158,14 @@ __device__ __forceinline__ void fma_lane(float (&a)[KK], float d, const float (&
 namespace spc {
 void note_launch(unsigned n = 1);
 
+// Per-(device, stream) block of device ints for the small selector / finite
+// flags the dispatchers pass between kernels on one stream (allocated once,
+// reused by every call on that stream: stream order makes the reuse safe).
+// Slots: see FLAG_* below.  nullptr if the allocation failed.
+int* stream_flags(cudaStream_t st);
+enum : int { FLAG_FINITE = 0, FLAG_CONV_SEL = 1, FLAG_BWW_SEL = 2, FLAG_TC_SEL2 = 3 /* 2 ints */,
+             FLAG_CONV_FINITE = 5, FLAG_COUNT = 64 };
+
 // Kernel attributes (cudaFuncSetAttribute) live in the device context, so a
 // "set once" guard must be per device: a process driving several GPUs sets
 // them on each.  Usage: `static PerDeviceOnce g; int d; if (g.needed(d)) {

@@ -52,23 +52,21 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
     if (g_math == SPC_MATH_TF32X3 && gate.in_ready == nullptr && tc_conv_supported(fwd, sh, V))
         return launch_tc_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);
     if (!force_generic && !pw_off && use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) {
-        int* finite = nullptr;
-        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
+        cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
         launch_finite_all(filt, (size_t)sh.K * sh.C, finite, st);
         e = launch_pw_gemm(fwd, sparse, sh, src, filt, dst, exec_ctr, finite, st, epi);
-        cudaFreeAsync(finite, st);
         return e;
     }
     if (!force_generic && !pw_off && pw_conv_supported(fwd, sh, V)) {
-        int* finite = nullptr;
-        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
+        cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
         launch_filter_finite(filt, (size_t)sh.K * sh.C, finite, st);
         e = launch_pw_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, finite, epi, gate);
         // filters with Inf/NaN: the per-element-skip tile kernel (exits otherwise)
         if (e == cudaSuccess) e = launch_tile_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi, finite, 0, gate);
-        cudaFreeAsync(finite, st);
         return e;
     }
     if (!force_generic && tile_conv_supported(fwd, sh, V))
@@ -86,12 +84,11 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
     if (g_math == SPC_MATH_TF32X3 && tc_bww_supported(sh, V))
         return launch_tc_bww(check_input, sparse, sh, chk, oth, dst, exec_ctr, st);
     if (!force_generic && !pw_off && pw_bww_supported(check_input, sh, V)) {
-        int* finite = nullptr;
-        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
+        cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
         launch_finite_all(oth, (size_t)sh.N * sh.K * sh.Hp * sh.Wp, finite, st);  // dY (ActNCHWc)
         e = launch_pw_bww(sparse, sh, chk, oth, dst, exec_ctr, finite, st);
-        cudaFreeAsync(finite, st);
         return e;
     }
     // V=16 tile kernels (tile_bww.cu).  SPC_ROW_BWW=1 selects the row-window
@@ -107,8 +104,8 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
     if (use_row || (!force_generic && tile_bww_supported(check_input, sh, V))) {
         const size_t chk_n = (size_t)((sh.N + 15) / 16) * 16 *
                              (check_input ? (size_t)sh.C * sh.H * sh.W : (size_t)sh.K * sh.Hp * sh.Wp);
-        int* finite = nullptr;
-        cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+        int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
+        cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
         launch_finite_all(chk, chk_n, finite, st);
         e = use_row ? launch_row_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, st)
@@ -123,7 +120,6 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
                 cudaFreeAsync(partial, st);
             }
         }
-        cudaFreeAsync(finite, st);
         return e;
     }
     const int splits = bww_generic_splits(sh);

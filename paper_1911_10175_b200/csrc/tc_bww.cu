@@ -643,8 +643,8 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
     // shape-general kernel otherwise (dispatch.cu launch_bww); sel2 = 0 (TC
     // ran), 1 (tile), 2 (generic)
     if (e == cudaSuccess) {
-        int* sel2 = nullptr;
-        e = cudaMallocAsync((void**)&sel2, 2 * sizeof(int), st);
+        int* sel2 = stream_flags(st) ? stream_flags(st) + FLAG_TC_SEL2 : nullptr;
+        e = sel2 ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e == cudaSuccess) {
             const size_t chk_n = (size_t)((sh.N + 15) / 16) * 16 *
                                  (check_input ? (size_t)sh.C * sh.H * sh.W : (size_t)sh.K * sh.Hp * sh.Wp);
@@ -662,7 +662,6 @@ cudaError_t launch_tc_bww(bool check_input, bool sparse, const DevShape& sh, con
                     cudaFreeAsync(gpart, st);
                 }
             }
-            cudaFreeAsync(sel2, st);
         }
     }
     cudaFreeAsync(scratch, st);

@@ -438,20 +438,28 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
     // (SPC_BWW_CTAS sweep, profiles/r01_tune.md).  Fixed per shape, so the
     // summation order stays deterministic.
     static const long env_ctas = std::getenv("SPC_BWW_CTAS") ? std::atol(std::getenv("SPC_BWW_CTAS")) : 0;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long target_ctas =
-        env_ctas > 0 ? env_ctas : (R == 3 && STR == 1 && base >= 16 && base <= 128) ? 148L * 18 : 148L * 6;
+        env_ctas > 0 ? env_ctas : (R == 3 && STR == 1 && base >= 16 && base <= 128) ? nsm * 18L : nsm * 6L;
     long splits = (target_ctas + base - 1) / base;
     if (splits > items) splits = items;
-    if (splits < 1) splits = 1;
     const size_t E = (size_t)Mc * R * S * Lc;
+    // bounded split-partial workspace: splits x |dG| <= 256 MB (stream-ordered pool memory)
+    const long cap = (long)((256ull << 20) / (E * sizeof(float)));
+    if (splits > cap) splits = cap;
+    if (splits < 1) splits = 1;
     float* partial = nullptr;
     cudaError_t e = cudaMallocAsync((void**)&partial, (size_t)splits * E * sizeof(float), st);
     if (e != cudaSuccess) return e;
     dim3 grid(Mc / G::NCH, Lc / (32 * KK), (unsigned)splits);
     if (sparse && JTSEL) {
-        int* sel = nullptr;
-        e = cudaMallocAsync((void**)&sel, sizeof(int), st);
-        if (e != cudaSuccess) return e;
+        int* sel = stream_flags(st) ? stream_flags(st) + FLAG_BWW_SEL : nullptr;
+        if (sel == nullptr) {
+            cudaFreeAsync(partial, st);
+            return cudaErrorMemoryAllocation;
+        }
         const size_t n = (size_t)((sh.N + 15) / 16) * Mc * (CI ? sh.H * sh.W : sh.Hp * sh.Wp) * 16;
         launch_density_probe(chk, n, 15, sel, st);
         auto k0 = bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, true>;
@@ -461,7 +469,6 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
         k0<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, sel, 0);
         k1<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, sel, 1);
         note_launch(2);
-        cudaFreeAsync(sel, st);
     } else {
         auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, true>
                            : bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, false>;
@@ -481,6 +488,7 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
     return e;
 }
 
+#ifdef SPC_DEV
 // Development entry: alternative BWW tile configurations (tools/tune.py --comp bww).
 cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, const DevShape& sh, const float* chk,
                                     const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
@@ -514,6 +522,7 @@ cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, 
     }
 #undef SPC_BV
 }
+#endif  // SPC_DEV
 
 bool tile_bww_supported(bool check_input, const DevShape& sh, int V) {
     if (V != 16) return false;

@@ -7,8 +7,10 @@ namespace spc {
 bool tile_bww_supported(bool check_input, const DevShape& sh, int V);
 cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, const float* chk, const float* oth,
                             float* dst, unsigned long long* exec_ctr, cudaStream_t st);
+#ifdef SPC_DEV
 cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, const DevShape& sh, const float* chk,
                                     const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st);
+#endif
 cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& sh, const float* chk,
                                  const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st,
                                  const int* sel, int want);

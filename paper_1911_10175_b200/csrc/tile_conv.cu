@@ -585,12 +585,15 @@ static cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* src,
     return cudaGetLastError();
 }
 
-// Development entry: time alternative tile configurations of the 3x3 s1
-// kernel (tools/tune.py).  Returns cudaErrorInvalidValue for an unknown or
-// inapplicable variant.
+// Development entry (include/spconv_b200_dev.h): run one tile configuration
+// of the 3x3 s1 kernel directly.  The product build keeps the branch /
+// jump-table configurations the tests compare bit for bit (2, 6, 14, 17, 41,
+// 42); the whole tuning table (tools/tune.py) needs `make DEV=1`.  Returns
+// cudaErrorInvalidValue for an unknown or inapplicable variant.
 cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const DevShape& sh, const float* src,
                                      const float* filt, float* dst, unsigned long long* exec_ctr, cudaStream_t st) {
     const int Co = fwd ? sh.K : sh.C;
+#ifdef SPC_DEV
     if (variant >= 50) {  // 1x1 stride 1 variants
         if (sh.R != 1 || sh.O != 1) return cudaErrorInvalidValue;
 #define SPC_V1(ID, KK, TH, TW, NWY, NWX)                                                                        \
@@ -621,6 +624,7 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
         }
 #undef SPC_V1
     }
+#endif
     if (sh.R != 3 || sh.O != 1) return cudaErrorInvalidValue;
 #define SPC_V(ID, KK, TH, TW, NWY, NWX, GPF) SPC_VJ(ID, KK, TH, TW, NWY, NWX, GPF, 0)
 #define SPC_VJ(ID, KK, TH, TW, NWY, NWX, GPF, JT)                                                               \
@@ -629,13 +633,18 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
         return fwd ? launch_cfg<true, KK, TH, TW, NWY, NWX, 3, 3, 1, GPF, JT>(sparse, sh, src, filt, dst, exec_ctr, st) \
                    : launch_cfg<false, KK, TH, TW, NWY, NWX, 3, 3, 1, GPF, JT>(sparse, sh, src, filt, dst, exec_ctr, st);
     switch (variant) {
+        SPC_V(2, 4, 4, 8, 2, 1, 1)
+        SPC_V(6, 2, 4, 8, 2, 2, 1)
+        SPC_VJ(14, 2, 4, 8, 2, 2, 1, 100)
+        SPC_VJ(17, 4, 4, 8, 2, 1, 1, 100)
+        SPC_VJ(41, 4, 4, 8, 1, 1, 1, 100)
+        SPC_V(42, 4, 7, 4, 1, 1, 1)
+#ifdef SPC_DEV
         SPC_V(0, 4, 4, 4, 2, 2, 1)
         SPC_V(1, 4, 4, 4, 2, 2, 0)
-        SPC_V(2, 4, 4, 8, 2, 1, 1)
         SPC_V(3, 4, 4, 8, 2, 1, 0)
         SPC_V(4, 4, 8, 4, 2, 1, 0)
         SPC_V(5, 2, 8, 8, 2, 1, 0)
-        SPC_V(6, 2, 4, 8, 2, 2, 1)
         SPC_V(7, 8, 4, 4, 2, 1, 0)
         SPC_V(8, 8, 2, 4, 2, 2, 0)
         SPC_V(9, 8, 2, 4, 2, 2, 1)
@@ -643,10 +652,8 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
         SPC_V(11, 4, 4, 4, 1, 4, 1)
         SPC_V(12, 2, 4, 8, 4, 1, 1)
         SPC_V(13, 4, 2, 8, 4, 1, 1)
-        SPC_VJ(14, 2, 4, 8, 2, 2, 1, 100)
         SPC_VJ(15, 2, 4, 8, 4, 1, 1, 100)
         SPC_VJ(16, 4, 4, 4, 2, 2, 1, 100)
-        SPC_VJ(17, 4, 4, 8, 2, 1, 1, 100)
         SPC_VJ(18, 4, 4, 8, 2, 1, 0, 100)
         SPC_VJ(19, 2, 4, 8, 2, 2, 0, 100)
         SPC_VJ(20, 2, 4, 8, 2, 2, 1, 15)
@@ -670,9 +677,8 @@ cudaError_t launch_tile_conv_variant(int variant, bool fwd, bool sparse, const D
         SPC_V(38, 4, 7, 4, 2, 1, 0)
         SPC_V(39, 4, 4, 7, 2, 1, 0)
         SPC_VJ(40, 4, 4, 8, 2, 2, 0, 100)
-        SPC_VJ(41, 4, 4, 8, 1, 1, 1, 100)
-        SPC_V(42, 4, 7, 4, 1, 1, 1)
         SPC_V(43, 4, 7, 4, 4, 1, 0)
+#endif
         default: return cudaErrorInvalidValue;
     }
 #undef SPC_V
@@ -756,8 +762,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
         if (sparse && kk4 && xsel == nullptr) {
             const int Ci = fwd ? sh.C : sh.K;
             const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
-            int* sel = nullptr;
-            cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
+            int* sel = stream_flags(st) ? stream_flags(st) + FLAG_CONV_SEL : nullptr;
+            cudaError_t e = sel ? cudaSuccess : cudaErrorMemoryAllocation;
             if (e != cudaSuccess) return e;
             // gated (host-buffer) launches sample only the first input chunk
             const size_t per_img = (size_t)Ci * Hs * Ws;
@@ -767,7 +773,6 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             if (e == cudaSuccess)
                 e = fwd ? launch_cfg<true, 4, 4, 8, 1, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
                         : launch_cfg<false, 4, 4, 8, 1, 1, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
-            cudaFreeAsync(sel, st);
             return e;
         }
         if (sparse && xsel == nullptr) {
@@ -777,8 +782,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             // 62.5, s=0.6 44 vs 59)
             const int Ci = fwd ? sh.C : sh.K;
             const int Hs = fwd ? sh.H : sh.Hp, Ws = fwd ? sh.W : sh.Wp;
-            int* sel = nullptr;
-            cudaError_t e = cudaMallocAsync((void**)&sel, sizeof(int), st);
+            int* sel = stream_flags(st) ? stream_flags(st) + FLAG_CONV_SEL : nullptr;
+            cudaError_t e = sel ? cudaSuccess : cudaErrorMemoryAllocation;
             if (e != cudaSuccess) return e;
             const size_t per_img = (size_t)Ci * Hs * Ws;
             launch_density_probe(src, per_img * (gate.in_ready ? (size_t)gate.ipc : (size_t)sh.N), 21, sel, st, gate);
@@ -787,7 +792,6 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
             if (e == cudaSuccess)
                 e = fwd ? launch_cfg<true, 2, 4, 8, 2, 2, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate)
                         : launch_cfg<false, 2, 4, 8, 2, 2, 3, 3, 1, 1, 100, true>(true, sh, src, filt, dst, exec_ctr, st, sel, 1, epi, gate);
-            cudaFreeAsync(sel, st);
             return e;
         }
         if (sparse) {
@@ -803,8 +807,8 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
                 // a stride-2 source pixel feeds ~2.25 taps: per-pixel branches cost more
                 // than the FMAs they skip, so finite filters run the counted-dense
                 // kernel (JT = 200); a filter with Inf/NaN keeps the per-pixel skip
-                int* finite = nullptr;
-                cudaError_t e = cudaMallocAsync((void**)&finite, sizeof(int), st);
+                int* finite = stream_flags(st) ? stream_flags(st) + FLAG_CONV_FINITE : nullptr;
+                cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
                 if (e != cudaSuccess) return e;
                 launch_finite_all(filt, (size_t)sh.K * sh.C * 9, finite, st);
                 if (kk4) {
@@ -820,7 +824,6 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
                         e = launch_cfg<true, 2, 4, 4, 2, 1, 3, 3, 2, 1, 0, true>(true, sh, src, filt, dst, exec_ctr,
                                                                                 st, finite, 0, epi, gate);
                 }
-                cudaFreeAsync(finite, st);
                 return e;
             }
             if (kk4) SPC_L(true, 4, 4, 4, 2, 1, 3, 2);

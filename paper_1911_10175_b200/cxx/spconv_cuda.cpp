@@ -103,6 +103,44 @@ bool native_backend_available(int V) { return spc_native_backend_available(V) !=
 
 std::vector<std::string> backend_names() { return {spc_backend_name()}; }
 
+namespace {
+// vec_probe holds plain function pointers without a width: one set per V.
+template <int V>
+lane_mask probe_cmp(const float* v) {
+    uint32_t m = 0;
+    check(spc_vector_probe(V, SPC_PROBE_CMP_NEQ_ZERO, v, nullptr, 0.0f, nullptr, &m));
+    return m;
+}
+template <int V>
+void probe_fma(float* acc, float s, const float* w) {
+    check(spc_vector_probe(V, SPC_PROBE_BROADCAST_FMA, acc, w, s, acc, nullptr));
+}
+template <int V>
+void probe_add(float* a, const float* b) {
+    check(spc_vector_probe(V, SPC_PROBE_ADD, a, b, 0.0f, a, nullptr));
+}
+template <int V>
+vec_probe make_probe() {
+    vec_probe p;
+    p.name = spc_backend_name();
+    p.width = V;
+    p.native = true;
+    p.cmp_neq_zero = &probe_cmp<V>;
+    p.broadcast_fma = &probe_fma<V>;
+    p.add = &probe_add<V>;
+    return p;
+}
+}  // namespace
+
+std::vector<vec_probe> vector_probes(int V) {
+    switch (V) {
+    case 4: return {make_probe<4>()};
+    case 8: return {make_probe<8>()};
+    case 16: return {make_probe<16>()};
+    default: throw error("vector_probes: V must be 4, 8 or 16");
+    }
+}
+
 conv_result sparse_fwd(const blocked_tensor& src, const blocked_tensor& filt, const conv_shape& shape,
                        const kernel_plan& pl, run_mode mode, int workers, backend_pref pref) {
     return run(component::fwd, src, filt, shape, pl, mode, workers, pref);

@@ -25,6 +25,9 @@ kernel_plan plan(const conv_shape& shape, component comp, int V, int register_bu
 
 bool native_backend_available(int V);
 std::vector<std::string> backend_names();
+// vector_probes (P/include/spconv/kernels.hpp:90-98): the device backend's
+// contract operations (spc_vector_probe), one warp, lane j = vector lane j.
+std::vector<vec_probe> vector_probes(int V);
 
 conv_result sparse_fwd(const blocked_tensor& src, const blocked_tensor& filt, const conv_shape& shape,
                        const kernel_plan& plan, run_mode mode, int workers = 1,

@@ -5,6 +5,8 @@
 // Exit status = number of failed checks.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <limits>
 #include <random>
 
 #include "spconv/kernels.hpp"
@@ -164,6 +166,39 @@ int main() {
         CHECK(throws([&] { cuda::plan(conv_shape::make(2, 16, 12, 6, 6, 3, 3, 1, 1), component::fwd, 8); }),
               "K not a multiple of V");
         CHECK(throws([&] { cuda::sparse_fwd(in.a, in.b, sh, pl, run_mode::sparse, 0); }), "workers = 0");
+    }
+    // vector_probes (kernels.hpp:90-98): the device backend's contract ops vs
+    // the reference's native backend on the same vectors (test_vec.cpp:38-57)
+    for (int V : {4, 8, 16}) {
+        const auto ours = cuda::vector_probes(V);
+        const auto refs = vector_probes(V);
+        CHECK(ours.size() == 1 && ours[0].width == V && ours[0].native, "vector_probes(%d) shape", V);
+        const vec_probe* rp = nullptr;
+        for (const auto& p : refs)
+            if (p.native) rp = &p;
+        if (!rp && !refs.empty()) rp = &refs.front();
+        std::mt19937_64 rng(V);
+        std::normal_distribution<float> nd(0.0f, 1.0f);
+        for (int t = 0; t < 20; ++t) {
+            float v[16], a[16], w[16], a2[16], b2[16];
+            for (int j = 0; j < V; ++j) {
+                v[j] = (rng() % 3 == 0) ? 0.0f : nd(rng);
+                a[j] = nd(rng);
+                w[j] = nd(rng);
+            }
+            v[0] = -0.0f;
+            if (V >= 8) { v[2] = std::numeric_limits<float>::quiet_NaN(); v[3] = std::numeric_limits<float>::infinity(); }
+            CHECK(ours[0].cmp_neq_zero(v) == rp->cmp_neq_zero(v), "cmp_neq_zero V=%d", V);
+            const float s = nd(rng);
+            std::memcpy(a2, a, sizeof(a));
+            ours[0].broadcast_fma(a, s, w);
+            rp->broadcast_fma(a2, s, w);
+            CHECK(std::memcmp(a, a2, V * sizeof(float)) == 0 || !rp->native, "broadcast_fma V=%d", V);
+            std::memcpy(b2, a, sizeof(a));
+            ours[0].add(a, w);
+            rp->add(b2, w);
+            CHECK(std::memcmp(a, b2, V * sizeof(float)) == 0, "add V=%d", V);
+        }
     }
     std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
     return g_fail;

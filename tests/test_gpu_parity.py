@@ -644,3 +644,21 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+def test_vector_probes_match_reference_semantics(sp):  # test_vec.cpp:38-57, kernels.hpp:90-98
+    rng = np.random.default_rng(8)
+    for V in (4, 8, 16):
+        (p,) = sp.vector_probes(V)
+        assert p.width == V and p.native
+        for _ in range(50):
+            v = rng.standard_normal(V).astype(np.float32)
+            v[rng.random(V) < 0.4] = 0.0
+            if V >= 8:
+                v[1], v[2], v[3] = -0.0, np.nan, np.inf
+            assert p.cmp_neq_zero(v) == O.cmp_neq_zero(v)
+            a, w = rng.standard_normal(V).astype(np.float32), rng.standard_normal(V).astype(np.float32)
+            s = np.float32(rng.standard_normal())
+            fused = (a.astype(np.float64) + np.float64(s) * w.astype(np.float64)).astype(np.float32)
+            assert np.array_equal(p.broadcast_fma(a, s, w), fused)
+            assert np.array_equal(p.add(a, w), (a + w).astype(np.float32))

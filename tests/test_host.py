@@ -28,8 +28,8 @@ REGISTRY = [
 ]
 
 
-def header_functions():
-    src = open(os.path.join(ROOT, "include", "spconv_b200.h")).read()
+def header_functions(name="spconv_b200.h"):
+    src = open(os.path.join(ROOT, "include", name)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(spc_[a-z0-9_]+)\s*\(", src)))
 
@@ -42,6 +42,10 @@ def test_library_exports_every_declared_symbol(sp):
         assert hasattr(lib, n), n
     assert set(names) == set(sp._lib.EXPORTED)
     assert lib.spc_abi_version() == 1
+    dev = header_functions("spconv_b200_dev.h")
+    assert set(dev) == set(sp._lib.DEV_EXPORTED)
+    for n in dev:
+        assert hasattr(lib, n), n
 
 
 def test_library_is_sm100a_only(sp):
