@@ -91,15 +91,24 @@ __global__ void __launch_bounds__(128) bww_generic_partial(DevShape sh, int V, c
     if (sel != nullptr && __ldg(sel) != want) return;
     const int Lc = CheckInput ? sh.K : sh.C;  // lane channel count
     const int Mc = CheckInput ? sh.C : sh.K;  // checked channel count
-    int b = blockIdx.x;
-    const int u = b % sh.R;
+    // grid-stride over the (m, v, u) x lane-block x split work units, so a
+    // gated launch that is not selected costs a small grid, not one CTA per unit
+    const int nlb = (Lc + blockDim.x - 1) / blockDim.x;
+    const long units = (long)Mc * sh.S * sh.R * nlb * splits;
+    for (long unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    long b = unit;
+    const int zsplit = (int)(b % splits);
+    b /= splits;
+    const int lb = (int)(b % nlb);
+    b /= nlb;
+    const int u = (int)(b % sh.R);
     b /= sh.R;
-    const int v = b % sh.S;
-    const int m = b / sh.S;
-    const int l = blockIdx.y * blockDim.x + threadIdx.x;
+    const int v = (int)(b % sh.S);
+    const int m = (int)(b / sh.S);
+    const int l = lb * blockDim.x + threadIdx.x;
     const bool active = l < Lc;
     const long rows = (long)sh.N * sh.Hp;
-    const long r0 = rows * blockIdx.z / splits, r1 = rows * (blockIdx.z + 1) / splits;
+    const long r0 = rows * zsplit / splits, r1 = rows * (zsplit + 1) / splits;
     float acc = 0.0f;
     unsigned cnt = 0;
     if (active) {
@@ -126,9 +135,10 @@ __global__ void __launch_bounds__(128) bww_generic_partial(DevShape sh, int V, c
         }
         const int k = CheckInput ? l : m, c = CheckInput ? m : l;
         const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
-        partial[(size_t)blockIdx.z * E + (((size_t)k * sh.C + c) * sh.S + v) * sh.R + u] = acc;
+        partial[(size_t)zsplit * E + (((size_t)k * sh.C + c) * sh.S + v) * sh.R + u] = acc;
     }
     warp_count_add(exec_ctr, (active && l % V == 0) ? cnt : 0u);
+    }
 }
 
 // Fixed-order split reduction + scatter into FilterKCRSblk (K, C).  This also
@@ -185,7 +195,8 @@ cudaError_t launch_bww_generic(bool check_input, bool sparse, const DevShape& sh
     const int Lc = check_input ? sh.K : sh.C;
     const int Mc = check_input ? sh.C : sh.K;
     const int bs = Lc >= 128 ? 128 : ((Lc + 31) / 32) * 32;
-    dim3 grid((unsigned)(Mc * sh.S * sh.R), (unsigned)((Lc + bs - 1) / bs), (unsigned)splits);
+    const long units = (long)Mc * sh.S * sh.R * ((Lc + bs - 1) / bs) * splits;
+    const unsigned grid = (unsigned)(units < 148L * 16 ? units : 148L * 16);
     if (check_input) {
         if (sparse) bww_generic_partial<true, true><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr, sel, want);
         else bww_generic_partial<true, false><<<grid, bs, 0, st>>>(sh, V, chk, oth, partial, splits, exec_ctr, sel, want);
@@ -197,7 +208,7 @@ cudaError_t launch_bww_generic(bool check_input, bool sparse, const DevShape& sh
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;
-    const unsigned rb = (unsigned)((E + 255) / 256 < 4096 ? (E + 255) / 256 : 4096);
+    const unsigned rb = (unsigned)((E + 255) / 256 < 148 * 4 ? (E + 255) / 256 : 148 * 4);
     bww_reduce_kernel<<<rb, 256, 0, st>>>(sh, V, partial, splits, dst, sel, want);
     note_launch();
     return cudaGetLastError();
