@@ -51,7 +51,13 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
     static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
     if (g_math == SPC_MATH_TF32X3 && gate.in_ready == nullptr && tc_conv_supported(fwd, sh, V))
         return launch_tc_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);
-    if (!force_generic && !pw_off && use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) {
+    // 1x1 stride-2 BWI: the tile kernel's per-pixel zero skip (every dY pixel
+    // feeds one dD pixel; the gap pixels are written as zeros) measured 1.65x
+    // faster than the GEMM kernels, at every sparsity (tools/skip_evidence.py,
+    // profiles/r02_skip_evidence.md); the other 1x1 passes run counted-dense GEMMs
+    const bool pw_s2_bwi = !fwd && sh.R == 1 && sh.S == 1 && sh.O == 2 && sh.P == 2;
+    const bool s2_bwi_tile = pw_s2_bwi && tile_conv_supported(fwd, sh, V);
+    if (!force_generic && !pw_off && !s2_bwi_tile && use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) {
         int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
         cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
@@ -59,7 +65,7 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
         e = launch_pw_gemm(fwd, sparse, sh, src, filt, dst, exec_ctr, finite, st, epi);
         return e;
     }
-    if (!force_generic && !pw_off && pw_conv_supported(fwd, sh, V)) {
+    if (!force_generic && !pw_off && !s2_bwi_tile && pw_conv_supported(fwd, sh, V)) {
         int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
         cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;

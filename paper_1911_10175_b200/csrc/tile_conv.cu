@@ -811,6 +811,10 @@ cudaError_t launch_tile_conv(bool fwd, bool sparse, const DevShape& sh, const fl
                 cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
                 if (e != cudaSuccess) return e;
                 launch_finite_all(filt, (size_t)sh.K * sh.C * 9, finite, st);
+                // SPC_FORCE_SKIP=1 runs the per-pixel-skip kernel for finite filters
+                // too (A/B evidence for the counted-dense choice, tools/skip_evidence.py)
+                static const bool force_skip = std::getenv("SPC_FORCE_SKIP") && std::atoi(std::getenv("SPC_FORCE_SKIP")) == 1;
+                if (force_skip) cudaMemsetAsync(finite, 0, sizeof(int), st);
                 if (kk4) {
                     e = launch_cfg<true, 4, 4, 4, 2, 1, 3, 3, 2, 1, 200, true>(true, sh, src, filt, dst, exec_ctr, st,
                                                                               finite, 1, epi, gate);
