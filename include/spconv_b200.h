@@ -4,7 +4,12 @@
  * Drop-in replacement for the hot path of the reference `spconv` library
  * (SparseTrain, arXiv 1911.10175): the three training passes FWD / BWI / BWW
  * over dense blocked fp32 tensors that skip work on zeros ReLU puts into the
- * checked tensor.  Every entry point below replaces one reference interface
+ * checked tensor.  Zero skipping is per element on 3x3 stride-1 passes, 3x3
+ * stride-2 BWI/BWW and 1x1 stride-2 BWI; 1x1 FWD/BWW, 1x1 stride-1 BWI and
+ * 3x3 stride-2 FWD execute every FMA ("counted dense": measured faster than
+ * any skip granularity on B200, profiles/r02_skip_evidence.md) with the
+ * reference's exact counters and Inf/NaN semantics.
+ * Every entry point below replaces one reference interface
  * (cited as P/<file>:<line>, P = /root/reference/proj):
  *
  *   spc_sparse_fwd      <- spconv::sparse_fwd    P/include/spconv/kernels.hpp:58-61

@@ -727,15 +727,30 @@ static spc_status run_fwd_bwi_gated(bool fwd, const spc_tensor* a, const spc_ten
     float *da = nullptr, *db = nullptr, *dd = nullptr;
     spc_counters* dc = nullptr;
     unsigned* flags = nullptr;  // in_ready[nc], done[nc], (unused)[nc], err
-    if ((e = cudaMallocAsync((void**)&da, a->numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&db, b->numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&dd, out.numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&dc, sizeof(spc_counters), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&flags, (3 * (size_t)nc + 1) * sizeof(unsigned), s0)) != cudaSuccess)
-        return cuda_fail(e, "alloc");
-    cudaMemsetAsync(flags, 0, (3 * (size_t)nc + 1) * sizeof(unsigned), s0);
-    cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, s0);
-    cudaEventRecord(hs->ready, s0);  // buffers, zeroed flags and the filter visible to the copy streams
+    cudaError_t ce = cudaSuccess;  // first failure of any copy / event call
+    auto ck = [&](cudaError_t x) {
+        if (x != cudaSuccess && ce == cudaSuccess) ce = x;
+    };
+    auto release = [&]() {
+        if (da) cudaFreeAsync(da, s0);
+        if (db) cudaFreeAsync(db, s0);
+        if (dd) cudaFreeAsync(dd, s0);
+        if (dc) cudaFreeAsync(dc, s0);
+        if (flags) cudaFreeAsync(flags, s0);
+    };
+    ck(cudaMallocAsync((void**)&da, a->numel * sizeof(float), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&db, b->numel * sizeof(float), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&dd, out.numel * sizeof(float), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&dc, sizeof(spc_counters), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&flags, (3 * (size_t)nc + 1) * sizeof(unsigned), s0));
+    if (ce != cudaSuccess) {
+        release();
+        cudaStreamSynchronize(s0);
+        return cuda_fail(ce, "alloc");
+    }
+    ck(cudaMemsetAsync(flags, 0, (3 * (size_t)nc + 1) * sizeof(unsigned), s0));
+    ck(cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, s0));
+    ck(cudaEventRecord(hs->ready, s0));  // buffers, zeroed flags and the filter visible to the copy streams
     Gate gate;
     gate.in_ready = flags;
     gate.done = flags + nc;
@@ -750,12 +765,12 @@ static spc_status run_fwd_bwi_gated(bool fwd, const spc_tensor* a, const spc_ten
         if ((e = cudaMallocHost((void**)&h_one, sizeof(unsigned))) != cudaSuccess) return cuda_fail(e, "pinned alloc");
         *h_one = 1u;
     }
-    cudaStreamWaitEvent(sin, hs->ready, 0);
+    ck(cudaStreamWaitEvent(sin, hs->ready, 0));
     for (int c = 0; c < nc; ++c) {
         const int i0 = c * ipc, i1 = i0 + ipc < N ? i0 + ipc : N;
-        cudaMemcpyAsync(da + (size_t)i0 * in_img, a->data + (size_t)i0 * in_img, (size_t)(i1 - i0) * in_img * sizeof(float),
-                        cudaMemcpyHostToDevice, sin);
-        cudaMemcpyAsync(const_cast<unsigned*>(gate.in_ready) + c, h_one, sizeof(unsigned), cudaMemcpyHostToDevice, sin);
+        ck(cudaMemcpyAsync(da + (size_t)i0 * in_img, a->data + (size_t)i0 * in_img, (size_t)(i1 - i0) * in_img * sizeof(float),
+                        cudaMemcpyHostToDevice, sin));
+        ck(cudaMemcpyAsync(const_cast<unsigned*>(gate.in_ready) + c, h_one, sizeof(unsigned), cudaMemcpyHostToDevice, sin));
     }
     // compute: one launch, gated per chunk
     spc_tensor ta = *a, tb = *b, td = out;
@@ -766,7 +781,7 @@ static spc_status run_fwd_bwi_gated(bool fwd, const spc_tensor* a, const spc_ten
     if (st == SPC_OK) {
         // copy-out: chunk c once its outputs are written
         // copy-out: poll the mapped words, issue chunk c's D2H as soon as it is written
-        cudaStreamWaitEvent(sout, hs->ready, 0);
+        ck(cudaStreamWaitEvent(sout, hs->ready, 0));
         for (int c = 0; c < nc; ++c) {
             const int i0 = c * ipc, i1 = i0 + ipc < N ? i0 + ipc : N;
             for (long spin = 0; !*(volatile unsigned*)(h_out + c); ++spin) {
@@ -775,26 +790,23 @@ static spc_status run_fwd_bwi_gated(bool fwd, const spc_tensor* a, const spc_ten
                     if (!*(volatile unsigned*)(h_out + c)) break;
                 }
             }
-            cudaMemcpyAsync(out.data + (size_t)i0 * out_img, dd + (size_t)i0 * out_img,
-                            (size_t)(i1 - i0) * out_img * sizeof(float), cudaMemcpyDeviceToHost, sout);
+            ck(cudaMemcpyAsync(out.data + (size_t)i0 * out_img, dd + (size_t)i0 * out_img,
+                            (size_t)(i1 - i0) * out_img * sizeof(float), cudaMemcpyDeviceToHost, sout));
         }
     }
     spc_counters hc{};
     unsigned herr = 0;
     if (st == SPC_OK) {
-        if (counters) cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s0);
-        cudaMemcpyAsync(&herr, gate.err, sizeof(herr), cudaMemcpyDeviceToHost, s0);
+        if (counters) ck(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s0));
+        ck(cudaMemcpyAsync(&herr, gate.err, sizeof(herr), cudaMemcpyDeviceToHost, s0));
     }
     cudaStreamSynchronize(sin);
     cudaStreamSynchronize(s0);
     cudaStreamSynchronize(sout);
-    cudaFreeAsync(da, s0);
-    cudaFreeAsync(db, s0);
-    cudaFreeAsync(dd, s0);
-    cudaFreeAsync(dc, s0);
-    cudaFreeAsync(flags, s0);
+    release();
     e = cudaStreamSynchronize(s0);
     if (st) return st;
+    if (ce != cudaSuccess) return cuda_fail(ce, "host run (copy / event)");
     if (e != cudaSuccess) return cuda_fail(e, "host run");
     if (herr) return fail(SPC_ERR_CUDA, "host run: an input chunk never arrived (gated launch timed out)");
     if (counters) *counters = hc;
@@ -855,16 +867,32 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     float *da = nullptr, *db = nullptr, *dd = nullptr, *dpart = nullptr;
     spc_counters* dc = nullptr;
     cudaError_t e;
-    if ((e = cudaMallocAsync((void**)&da, a->numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&db, b->numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&dd, out.numel * sizeof(float), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if ((e = cudaMallocAsync((void**)&dc, nc * sizeof(spc_counters), s0)) != cudaSuccess) return cuda_fail(e, "alloc");
-    if (bww && nc > 1 &&
-        (e = cudaMallocAsync((void**)&dpart, (size_t)nc * out.numel * sizeof(float), s0)) != cudaSuccess)
-        return cuda_fail(e, "alloc");
+    // every CUDA call's status is kept (the first failure wins) and checked
+    // before the chunk loop goes on; allocations are released on every path
+    cudaError_t ce = cudaSuccess;
+    auto ck = [&](cudaError_t x) {
+        if (x != cudaSuccess && ce == cudaSuccess) ce = x;
+    };
+    auto release = [&]() {
+        if (da) cudaFreeAsync(da, s0);
+        if (db) cudaFreeAsync(db, s0);
+        if (dd) cudaFreeAsync(dd, s0);
+        if (dc) cudaFreeAsync(dc, s0);
+        if (dpart) cudaFreeAsync(dpart, s0);
+    };
+    ck(cudaMallocAsync((void**)&da, a->numel * sizeof(float), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&db, b->numel * sizeof(float), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&dd, out.numel * sizeof(float), s0));
+    if (ce == cudaSuccess) ck(cudaMallocAsync((void**)&dc, nc * sizeof(spc_counters), s0));
+    if (ce == cudaSuccess && bww && nc > 1) ck(cudaMallocAsync((void**)&dpart, (size_t)nc * out.numel * sizeof(float), s0));
+    if (ce != cudaSuccess) {
+        release();
+        cudaStreamSynchronize(s0);
+        return cuda_fail(ce, "alloc");
+    }
     // operands that are not batch-sliced go first, on s0
-    if (!bww) cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, s0);
-    cudaEventRecord(hs->ready, s0);  // allocations (+ filter) visible to the other streams
+    if (!bww) ck(cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, s0));
+    ck(cudaEventRecord(hs->ready, s0));  // allocations (+ filter) visible to the other streams
 
     const float* hchk = chk->data;
     float* dchk = chk == a ? da : db;
@@ -880,21 +908,21 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     // kernel and chunk c-1's D2H run at once and PCIe carries both directions
     // together (measured duplex 82-91 GB/s vs 55-57 one way).
     cudaStream_t sin = hs->s[1], sout = hs->s[2];
-    cudaStreamWaitEvent(sin, hs->ready, 0);
-    for (int c = 0; c < nc && st == SPC_OK; ++c) {
+    ck(cudaStreamWaitEvent(sin, hs->ready, 0));
+    for (int c = 0; c < nc && st == SPC_OK && ce == cudaSuccess; ++c) {
         const int u0 = (int)((long)units * c / nc), u1 = (int)((long)units * (c + 1) / nc);
         const int i0 = bww ? u0 * V : u0;
         const int i1 = bww ? (u1 * V < shape->N ? u1 * V : shape->N) : u1;
         spc_shape shc = *shape;
         shc.N = i1 - i0;
         // H2D of this chunk's slices
-        cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
-                        (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin);
+        ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
+                        (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
         if (oth)
-            cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
-                            (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sin);
-        cudaEventRecord(hs->in_done[c], sin);
-        cudaStreamWaitEvent(s0, hs->in_done[c], 0);
+            ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
+                            (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        ck(cudaEventRecord(hs->in_done[c], sin));
+        ck(cudaStreamWaitEvent(s0, hs->in_done[c], 0));
         // chunk tensor descriptors
         spc_tensor tchk = *chk, toth, tb = *b, td = out;
         tchk.data = dchk + (size_t)u0 * chk_unit;
@@ -918,32 +946,30 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
             st = plan->comp == SPC_FWD ? spc_sparse_fwd(&tchk, &tb, &shc, plan, mode, &td, counters ? dc + c : nullptr, s0)
                                        : spc_sparse_bwi(&tchk, &tb, &shc, plan, mode, &td, counters ? dc + c : nullptr, s0);
             if (st == SPC_OK) {
-                cudaEventRecord(hs->k_done[c], s0);
-                cudaStreamWaitEvent(sout, hs->k_done[c], 0);
-                cudaMemcpyAsync(out.data + (size_t)i0 * out_unit, td.data, td.numel * sizeof(float),
-                                cudaMemcpyDeviceToHost, sout);
+                ck(cudaEventRecord(hs->k_done[c], s0));
+                ck(cudaStreamWaitEvent(sout, hs->k_done[c], 0));
+                ck(cudaMemcpyAsync(out.data + (size_t)i0 * out_unit, td.data, td.numel * sizeof(float),
+                                cudaMemcpyDeviceToHost, sout));
             }
         }
     }
-    if (st == SPC_OK && bww) {
+    if (st == SPC_OK && ce == cudaSuccess && bww) {
         // reduce the chunks' partial dG in fixed order on the compute stream, copy dG out
         if (nc > 1) {
             sum_partials_kernel<<<grid_for(out.numel), 256, 0, s0>>>(dpart, nc, out.numel, dd);
             note_launch();
+            ck(cudaGetLastError());
         }
-        cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0);
+        ck(cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0));
     }
     spc_counters hc[kMaxHostChunks];
     if (st == SPC_OK && counters)
-        cudaMemcpyAsync(hc, dc, nc * sizeof(spc_counters), cudaMemcpyDeviceToHost, s0);
+        ck(cudaMemcpyAsync(hc, dc, nc * sizeof(spc_counters), cudaMemcpyDeviceToHost, s0));
     for (int c = 0; c < 3; ++c) cudaStreamSynchronize(hs->s[c]);
-    cudaFreeAsync(da, s0);
-    cudaFreeAsync(db, s0);
-    cudaFreeAsync(dd, s0);
-    cudaFreeAsync(dc, s0);
-    if (dpart) cudaFreeAsync(dpart, s0);
+    release();
     e = cudaStreamSynchronize(s0);
     if (st) return st;
+    if (ce != cudaSuccess) return cuda_fail(ce, "host run (copy / event)");
     if (e != cudaSuccess) return cuda_fail(e, "host run");
     if (counters) {
         std::memset(counters, 0, sizeof(*counters));

@@ -34,7 +34,11 @@ def summarize(rep):
     else:
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    return [summarize_row(rep, hdr, units, vals) for vals in rows[2:]]
+
+
+def summarize_row(rep, hdr, units, vals):
     out = {"report": rep.split("/")[-1], "kernel": vals[hdr.index("Kernel Name")][:160]}
     stalls = {}
     for h, u, v in zip(hdr, units, vals):
@@ -62,7 +66,7 @@ def summarize(rep):
 
 
 if __name__ == "__main__":
-    res = [summarize(p) for p in sys.argv[2:]]
+    res = [r for p in sys.argv[2:] for r in summarize(p)]
     json.dump(res, open(sys.argv[1], "w"), indent=1)
     for r in res:
         print(json.dumps({k: r[k] for k in r if k != "stall_mix_pct"}))
