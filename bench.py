@@ -249,6 +249,7 @@ def config_dict(args, ws):
 
 
 SPARSITY_NOTE = {
+    "cfg1_single3x3_b16": "D: i.i.d. ReLU(N(-t,1)) at 0.5; dY: N(0,1) x independent 50% Bernoulli mask (seed 0)",
     "resnet34_b64": "D: per-layer i.i.d. s_l ~ U[0.4, 0.8] (seeded); dY dense (BatchNorm)",
     "resnet50_b64": "D: spatially correlated ReLU(conv3x3_rand(N(0,1)) - tau), mean 0.6; dY dense (BatchNorm)",
     "fixup_resnet50_b256": "ReLU masks of the chain's own seeded forward pass (~0.7 activation sparsity)",

@@ -160,7 +160,7 @@ def relu_threshold(s: float) -> float:
 
 
 # ---------------------------------------------------------------- per-config inputs
-GRID_CONFIGS = ("cfg1_single3x3_b16", "vgg16_b32")   # i.i.d. D and masked dY at a swept s
+GRID_CONFIGS = ("vgg16_b32",)  # i.i.d. D and masked dY swept over the sparsity grid (cfg 1: fixed s = 0.5)
 BN_CONFIGS = ("resnet34_b64", "resnet50_b64")         # dense dY (BatchNorm before the ReLU)
 R50_TARGET = 0.6
 
