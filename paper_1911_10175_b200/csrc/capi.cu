@@ -13,7 +13,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <random>
-#include <mutex>
 #include <map>
 #include <mutex>
 #include <string>
@@ -23,6 +22,8 @@
 #include "dispatch.h"
 #include "tile_bww.h"
 #include "tile_conv.h"
+#include "host_stage.h"
+#include "../../include/spconv_b200_dev.h"
 
 namespace spc {
 
@@ -837,7 +838,8 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     // launch is an FFMA tile kernel: the tensor-core arithmetic keeps the
     // chunked path, so the host and device paths compute alike.
     static const bool gate_on = std::getenv("SPC_HOST_GATE") && std::atoi(std::getenv("SPC_HOST_GATE")) == 1;
-    if (plan->comp != SPC_BWW && gate_on && math_mode() == SPC_MATH_FP32 &&
+    if (plan->comp != SPC_BWW && gate_on && math_mode() == SPC_MATH_FP32 && !is_pageable(a->data) &&
+        !is_pageable(out.data) &&
         conv_supports_gate(plan->comp == SPC_FWD, make_dev_shape(*shape), plan->V)) {
         st = run_fwd_bwi_gated(plan->comp == SPC_FWD, a, b, *shape, *plan, mode, out, counters, hs);
         if (st == SPC_OK) *dst = out;
@@ -902,6 +904,38 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     const size_t oth_unit = oth ? oth->numel / shape->N : 0;   // per image (NCHWc)
     const size_t out_unit = bww ? 0 : out.numel / shape->N;    // per image
 
+    // Pageable host buffers (a std::vector caller): the batch-sliced inputs are
+    // copied by host threads into two pinned slots and DMA'd from there, the
+    // outputs DMA'd into two pinned slots and copied out by the host, so the
+    // host copy of chunk c+1 overlaps chunk c's DMA and kernel (host_stage.cu).
+    const bool stage_in = is_pageable(hchk) || (oth && is_pageable(hoth));
+    const bool stage_out = is_pageable(out.data);
+    HostStaging& stg = host_staging();
+    size_t in_max = 0, out_max = bww ? out.numel * sizeof(float) : 0;
+    for (int c = 0; c < nc; ++c) {
+        const int u0 = (int)((long)units * c / nc), u1 = (int)((long)units * (c + 1) / nc);
+        const int i0 = bww ? u0 * V : u0;
+        const int i1 = bww ? (u1 * V < shape->N ? u1 * V : shape->N) : u1;
+        const size_t ib = ((size_t)(u1 - u0) * chk_unit + (size_t)(i1 - i0) * oth_unit) * sizeof(float);
+        if (ib > in_max) in_max = ib;
+        if (!bww && (size_t)(i1 - i0) * out_unit * sizeof(float) > out_max) out_max = (size_t)(i1 - i0) * out_unit * sizeof(float);
+    }
+    if (stage_in || stage_out) {
+        ck(stg.reserve(stage_in ? in_max : 0, stage_out ? out_max : 0));
+        if (ce != cudaSuccess) {
+            release();
+            cudaStreamSynchronize(s0);
+            return cuda_fail(ce, "pinned staging");
+        }
+    }
+    // a finished D2H chunk into a pinned slot -> the caller's pageable output
+    auto drain_out = [&](int c) {
+        const int u0 = (int)((long)units * c / nc), u1 = (int)((long)units * (c + 1) / nc);
+        ck(cudaEventSynchronize(stg.out_ev[c & 1]));
+        if (ce == cudaSuccess)
+            host_copy(out.data + (size_t)u0 * out_unit, stg.out[c & 1], (size_t)(u1 - u0) * out_unit * sizeof(float));
+    };
+
     // Three engines, three streams: every H2D on the copy-in stream back to
     // back, every kernel on the compute stream, every D2H on the copy-out
     // stream, joined per chunk by events -- so chunk c+1's H2D, chunk c's
@@ -916,11 +950,25 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
         spc_shape shc = *shape;
         shc.N = i1 - i0;
         // H2D of this chunk's slices
-        ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
-                        (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
-        if (oth)
-            ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
-                            (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        const size_t cb = (size_t)(u1 - u0) * chk_unit * sizeof(float), ob = (size_t)(i1 - i0) * oth_unit * sizeof(float);
+        if (stage_in) {
+            float* slot = stg.in[c & 1];
+            if (c >= 2) ck(cudaEventSynchronize(stg.in_ev[c & 1]));  // chunk c-2's H2D has read the slot
+            if (ce != cudaSuccess) break;
+            host_copy(slot, hchk + (size_t)u0 * chk_unit, cb);
+            if (oth) host_copy(reinterpret_cast<char*>(slot) + cb, hoth + (size_t)i0 * oth_unit, ob);
+            ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, slot, cb, cudaMemcpyHostToDevice, sin));
+            if (oth)
+                ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, reinterpret_cast<char*>(slot) + cb, ob,
+                                   cudaMemcpyHostToDevice, sin));
+            ck(cudaEventRecord(stg.in_ev[c & 1], sin));
+        } else {
+            ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit, cb, cudaMemcpyHostToDevice,
+                               sin));
+            if (oth)
+                ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit, ob,
+                                   cudaMemcpyHostToDevice, sin));
+        }
         ck(cudaEventRecord(hs->in_done[c], sin));
         ck(cudaStreamWaitEvent(s0, hs->in_done[c], 0));
         // chunk tensor descriptors
@@ -948,11 +996,20 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
             if (st == SPC_OK) {
                 ck(cudaEventRecord(hs->k_done[c], s0));
                 ck(cudaStreamWaitEvent(sout, hs->k_done[c], 0));
-                ck(cudaMemcpyAsync(out.data + (size_t)i0 * out_unit, td.data, td.numel * sizeof(float),
-                                cudaMemcpyDeviceToHost, sout));
+                if (stage_out) {
+                    // the slot was emptied by drain_out(c - 2) in iteration c - 1
+                    ck(cudaMemcpyAsync(stg.out[c & 1], td.data, td.numel * sizeof(float), cudaMemcpyDeviceToHost,
+                                       sout));
+                    ck(cudaEventRecord(stg.out_ev[c & 1], sout));
+                    if (c >= 1) drain_out(c - 1);
+                } else {
+                    ck(cudaMemcpyAsync(out.data + (size_t)i0 * out_unit, td.data, td.numel * sizeof(float),
+                                       cudaMemcpyDeviceToHost, sout));
+                }
             }
         }
     }
+    if (stage_out && !bww && st == SPC_OK && ce == cudaSuccess) drain_out(nc - 1);
     if (st == SPC_OK && ce == cudaSuccess && bww) {
         // reduce the chunks' partial dG in fixed order on the compute stream, copy dG out
         if (nc > 1) {
@@ -960,7 +1017,13 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
             note_launch();
             ck(cudaGetLastError());
         }
-        ck(cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0));
+        if (stage_out) {
+            ck(cudaMemcpyAsync(stg.out[0], dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0));
+            ck(cudaStreamSynchronize(s0));
+            if (ce == cudaSuccess) host_copy(out.data, stg.out[0], out.numel * sizeof(float));
+        } else {
+            ck(cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, s0));
+        }
     }
     spc_counters hc[kMaxHostChunks];
     if (st == SPC_OK && counters)

@@ -136,9 +136,9 @@ __device__ __forceinline__ void warp_count_add(unsigned long long* ctr, unsigned
 #ifndef SPC_FFMA2_MIN
 #define SPC_FFMA2_MIN 16  // minimum FMAs per lane in a pixel block for the packed form
 #endif
-template <int KK>
+template <int KK, int MIN = SPC_FFMA2_MIN>
 __device__ __forceinline__ void fma_lane(float (&a)[KK], float d, const float (&g)[KK], int ntap) {
-    if (SPC_FFMA2 && KK >= 4 && ntap * KK >= SPC_FFMA2_MIN) {
+    if (SPC_FFMA2 && KK >= 4 && ntap * KK >= MIN) {
         const float2 dd = make_float2(d, d);
 #pragma unroll
         for (int j = 0; j < KK; j += 2) {

@@ -518,6 +518,14 @@ cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, 
         SPC_BV(22, false, 4, 1, 8, 4, 4)
         SPC_BV(23, false, 2, 1, 8, 4, 7)
         SPC_BV(24, false, 4, 1, 4, 2, 4)
+        // round 2: more checked channels per warp (CB) against the shared-memory bound
+        SPC_BV(30, true, 4, 2, 8, 7, 4)
+        SPC_BV(31, true, 4, 2, 4, 7, 4)
+        SPC_BV(32, true, 2, 4, 4, 7, 4)
+        SPC_BV(33, true, 2, 4, 8, 7, 4)
+        SPC_BV(34, true, 2, 2, 8, 7, 4)
+        SPC_BV(35, true, 4, 2, 8, 4, 4)
+        SPC_BV(36, true, 4, 3, 8, 4, 4)
         default: return cudaErrorInvalidValue;
     }
 #undef SPC_BV

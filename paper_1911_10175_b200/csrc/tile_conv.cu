@@ -27,6 +27,15 @@
 #include <type_traits>
 
 #include "common.cuh"
+
+// Minimum FMAs per lane in a pixel block for the packed form in the in-line
+// (branch) loop.  16 keeps 1-3-tap blocks (image-border region pixels) as a
+// branch + scalar FFMAs; 4 (every KK=4 block FFMA2, 2-6 instructions that ptxas
+// if-converts) measured 7-12% SLOWER on VGG16 conv2_2-conv5_2 at s = 0.4 / 0.6
+// (round 2, A/B on one box): predicated-off FFMA2s still occupy the FMA pipe.
+#ifndef SPC_CONV_FFMA2_MIN
+#define SPC_CONV_FFMA2_MIN 16
+#endif
 #include "jt_blocks.cuh"
 #include "pw_bww.h"
 #include "tile_conv.h"
@@ -446,7 +455,7 @@ __device__ __forceinline__ void tile_conv_body(DevShape sh, const float* __restr
                             for (int u = 0; u < R; ++u) {
                                 const int tx = AX::target(rx, u);
                                 if (tx < 0) continue;
-                                fma_lane(acc[ty * TW + tx], d, g[v * R + u].v, ntap);
+                                fma_lane<KK, SPC_CONV_FFMA2_MIN>(acc[ty * TW + tx], d, g[v * R + u].v, ntap);
                             }
                         }
                     }

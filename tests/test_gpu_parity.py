@@ -424,16 +424,22 @@ def test_host_path_pipelined_chunks_match_device_path(sp):
         a, b, ba, bb = make_inputs(sp, sh, comp, check, 0.6, V, 11)
         pl = sp.plan(sh, sp.Component(comp), V, 30, sp.BwwCheck(check))
         rd = sp.run_parallel(ba, bb, sh, pl, sp.RunMode.sparse)
-        ha, hb = ba.to(None), bb.to(None)
-        rh = sp.run_parallel(ha, hb, sh, pl, sp.RunMode.sparse)
-        got, ref = rh.out.data, rd.out.data.cpu().numpy()
-        if comp == 2:
-            # Two GPU summation orders (chunked vs whole-batch split reduction);
-            # each is separately within 1e-5 of the oracle (test_bww_*).
-            assert O.max_abs_rel(got, ref) <= 2e-6
-        else:
-            assert np.array_equal(got, ref)
-        assert rh.counters == rd.counters
+        ha, hb = ba.to(None), bb.to(None)  # pageable numpy: the pinned staging ring (host_stage.cu)
+        import torch
+        pa = sp.BlockedTensor(**{**ha.header(), "data": torch.from_numpy(ha.data).pin_memory().numpy()})
+        pb = sp.BlockedTensor(**{**hb.header(), "data": torch.from_numpy(hb.data).pin_memory().numpy()})
+        runs = [sp.run_parallel(ha, hb, sh, pl, sp.RunMode.sparse), sp.run_parallel(pa, pb, sh, pl, sp.RunMode.sparse)]
+        ref = rd.out.data.cpu().numpy()
+        for rh in runs:
+            got = rh.out.data
+            if comp == 2:
+                # Two GPU summation orders (chunked vs whole-batch split reduction);
+                # each is separately within 1e-5 of the oracle (test_bww_*).
+                assert O.max_abs_rel(got, ref) <= 2e-6
+            else:
+                assert np.array_equal(got, ref)
+            assert rh.counters == rd.counters
+        assert np.array_equal(runs[0].out.data, runs[1].out.data)  # pageable == pinned, bitwise
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
