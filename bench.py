@@ -377,7 +377,7 @@ def main():
     def dg_alloc(n):
         start = cursor[0]
         cursor[0] += n
-        return dg_buf.slice(start, n) if comm is not None else dg_buf[start:start + n]
+        return dg_buf.slice(start, n) if hasattr(dg_buf, "slice") else dg_buf[start:start + n]
 
     work = build_work(args, sp, wl, dev, n_local, rank, dg_alloc)
     torch.cuda.synchronize()

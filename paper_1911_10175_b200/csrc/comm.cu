@@ -197,13 +197,14 @@ spc_status spc_comm_window_alloc(spc_comm* comm, size_t bytes, void** ptr, int* 
     if (ncclResult_t r = nccl().MemAlloc(&p, bytes ? bytes : 4)) return nccl_fail(r, "ncclMemAlloc");
     ncclWindow_t win = nullptr;
     int sym = 0;
-    if (nccl().WindowRegister) {
-        if (ncclResult_t r = nccl().WindowRegister(comm->nc, p, bytes ? bytes : 4, &win, NCCL_WIN_COLL_SYMMETRIC)) {
-            nccl().MemFree(p);
-            return nccl_fail(r, "ncclCommWindowRegister");
-        }
+    // The window is an optimisation (NCCL's symmetric kernels); where the
+    // library or the system cannot register one, the buffer stays plain
+    // ncclMemAlloc memory and the allreduce takes NCCL's regular path.
+    if (nccl().WindowRegister &&
+        nccl().WindowRegister(comm->nc, p, bytes ? bytes : 4, &win, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess)
         sym = 1;
-    }
+    else
+        win = nullptr;
     {
         std::lock_guard<std::mutex> g(comm->mu);
         comm->wins.push_back({p, bytes, win});

@@ -157,11 +157,16 @@ class Comm:
         if st:
             raise SpconvError(st, _lib.last_error())
 
-    def window(self, numel: int) -> tuple[DeviceBuffer, bool]:
-        """Collective: a float32 device buffer in an NCCL symmetric window."""
+    def window(self, numel: int):
+        """Collective: a float32 device buffer in an NCCL symmetric window
+        (``(DeviceBuffer, True)``); where NCCL cannot provide one, plain NCCL
+        memory (``(DeviceBuffer, False)``) or, if even that fails, a torch
+        CUDA tensor (``(tensor, False)``) -- the allreduce works on all three."""
         C = self._C
         p, sym = C.c_void_p(), C.c_int()
-        self._check(self.L.spc_comm_window_alloc(self.h, 4 * numel, C.byref(p), C.byref(sym)))
+        if self.L.spc_comm_window_alloc(self.h, 4 * numel, C.byref(p), C.byref(sym)) != 0:
+            import torch
+            return torch.zeros(numel, dtype=torch.float32, device="cuda"), False
         buf = DeviceBuffer(p.value, numel, self)
         self._windows.append(p)
         return buf, bool(sym.value)
