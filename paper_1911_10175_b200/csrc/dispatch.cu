@@ -97,16 +97,18 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
         e = launch_pw_bww(sparse, sh, chk, oth, dst, exec_ctr, finite, st);
         return e;
     }
-    // V=16 tile kernels (tile_bww.cu).  SPC_ROW_BWW=1 selects the row-window
-    // kernel for 3x3 s1 check=input instead (row_bww.cu: measured 8-30%
-    // slower than the tile kernel on the VGG layers except conv1_2, kept for
-    // A/B).  Both add d * 0 for taps whose partner pixel lies
+    // V=16 tile kernels (tile_bww.cu), except 3x3 s1 check=input with 64-channel
+    // lane blocks (K % 128 != 0: VGG conv1_2, ResNet stage 1), where the
+    // row-window kernel (row_bww.cu, KK=2) measured 4-22% faster at every
+    // sparsity; on the 128-multiple layers it is 8-30% slower.
+    // SPC_ROW_BWW=0 / 1 forces the tile / row kernel (A/B).  Both add d * 0 for taps whose partner pixel lies
     // outside the image (zero-filled staging), exact only for a FINITE checked
     // tensor: a device scan of it picks, for Inf/NaN, the shape-general
     // kernel (exact skips, P/src/kernel_impl.hpp:239-304).  All are enqueued;
     // the non-matching ones exit at entry (no host sync).
-    static const bool row_on = std::getenv("SPC_ROW_BWW") && std::atoi(std::getenv("SPC_ROW_BWW")) == 1;
-    const bool use_row = !force_generic && row_on && row_bww_supported(check_input, sh, V);
+    static const int row_env = std::getenv("SPC_ROW_BWW") ? std::atoi(std::getenv("SPC_ROW_BWW")) : -1;
+    const bool row_pick = row_env == 1 || (row_env == -1 && sh.K % 128 != 0);
+    const bool use_row = !force_generic && row_pick && row_bww_supported(check_input, sh, V);
     if (use_row || (!force_generic && tile_bww_supported(check_input, sh, V))) {
         const size_t chk_n = (size_t)((sh.N + 15) / 16) * 16 *
                              (check_input ? (size_t)sh.C * sh.H * sh.W : (size_t)sh.K * sh.Hp * sh.Wp);
