@@ -23,6 +23,7 @@
 #include "tile_bww.h"
 #include "tile_conv.h"
 #include "host_stage.h"
+#include <nvtx3/nvToolsExt.h>
 #include "../../include/spconv_b200_dev.h"
 
 namespace spc {
@@ -570,14 +571,24 @@ spc_status spc_analytic_counters(const spc_shape* shape, const spc_plan* plan, i
     return SPC_OK;
 }
 
+// NVTX ranges around the entry points (tracing): the names show up
+// in Nsight Systems / ncu --nvtx timelines; without a tool attached the push
+// and pop are a cheap no-op (nvtx3 is header-only, no link dependency).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 spc_status spc_sparse_fwd(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
                           const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    NvtxRange r("spc_sparse_fwd");
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
     return run_fwd_bwi(true, src, filt, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
 }
 
 spc_status spc_sparse_bwi(const spc_tensor* grad_out, const spc_tensor* filt_t, const spc_shape* shape,
                           const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    NvtxRange r("spc_sparse_bwi");
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
     return run_fwd_bwi(false, grad_out, filt_t, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
 }
@@ -591,6 +602,7 @@ static spc_status check_epi(const spc_epilogue* epi) {
 spc_status spc_sparse_fwd_ex(const spc_tensor* src, const spc_tensor* filt, const spc_shape* shape,
                              const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
                              spc_counters* d_counters, void* stream) {
+    NvtxRange r("spc_sparse_fwd_ex");
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
     spc_status s = check_epi(epi);
     if (s) return s;
@@ -600,6 +612,7 @@ spc_status spc_sparse_fwd_ex(const spc_tensor* src, const spc_tensor* filt, cons
 spc_status spc_sparse_bwi_ex(const spc_tensor* grad_out, const spc_tensor* filt_t, const spc_shape* shape,
                              const spc_plan* plan, int mode, const spc_epilogue* epi, spc_tensor* dst,
                              spc_counters* d_counters, void* stream) {
+    NvtxRange r("spc_sparse_bwi_ex");
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
     spc_status s = check_epi(epi);
     if (s) return s;
@@ -625,6 +638,7 @@ spc_status spc_epilogue_apply(const spc_epilogue* epi, float* data, size_t n, vo
 
 spc_status spc_sparse_bww(const spc_tensor* input, const spc_tensor* grad_out, const spc_shape* shape,
                           const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* d_counters, void* stream) {
+    NvtxRange r("spc_sparse_bww");
     if (!shape || !plan) return fail(SPC_ERR_ARG, "null shape or plan");
     return run_bww(input, grad_out, *shape, *plan, mode, dst, d_counters, (cudaStream_t)stream);
 }
@@ -816,6 +830,7 @@ static spc_status run_fwd_bwi_gated(bool fwd, const spc_tensor* a, const spc_ten
 
 spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters) {
+    NvtxRange r("spc_run_parallel_host");
     if (!a || !b || !shape || !plan || !dst) return fail(SPC_ERR_ARG, "null argument");
     spc_status st;
     switch (plan->comp) {
