@@ -39,7 +39,7 @@ def main():
 
     import paper_1911_10175_b200 as sp
     from paper_1911_10175_b200 import chain as CH
-    from paper_1911_10175_b200.dist import GradAllreduce, shard_range
+    from paper_1911_10175_b200.dist import Comm, CommAllreduce, shard_range
 
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -52,7 +52,9 @@ def main():
     sp.set_math(sp.Math[a.math])
     _, n_local = shard_range(a.batch, ws, rank)
     t0 = time.time()
-    ar = GradAllreduce(device=dev) if distributed else None
+    # the product's NCCL communicator (csrc/comm.cu): per-block dG allreduce on a side stream
+    comm = Comm() if distributed else None
+    ar = CommAllreduce(comm, dev) if comm is not None else None
     # one seed on every rank: the same weights, each rank its slice of the global batch
     ch = CH.fixup_resnet50(a.batch, scale=a.scale, seed=1234, mode=sp.RunMode[a.mode], allreduce=ar,
                            x_sparsity=a.x_sparsity, world=ws, rank=rank)
@@ -98,6 +100,7 @@ def main():
         os.write(_OUT, (json.dumps(out) + "\n").encode())
     if distributed:
         dist.barrier()
+        comm.close()
         dist.destroy_process_group()
 
 
