@@ -16,9 +16,10 @@ Per configuration (``layer_inputs_host`` / ``layer_inputs_device``):
   conv and its ReLU, so the conv's output gradient carries no ReLU zeros
   (the reference projector's rule, P/src/projector.cpp:120-125).
 * cfg 4 (ResNet-50): spatially correlated D = ReLU(conv3x3_rand(X) - tau),
-  X ~ N(0,1), random He-normal C->C weights, tau the 0.6-quantile of the
-  conv output (estimated on a seeded sample) => mean sparsity 0.6 with zeros
-  clustered in space and in channels; dY dense N(0,1) (BatchNorm, as cfg 3).
+  X ~ N(0,1), random C->C weights built on a smoothing kernel (see
+  spatial_activation), tau the 0.6-quantile of the conv output (estimated on
+  a seeded sample) => mean sparsity 0.6 with zeros clustered in space;
+  dY dense N(0,1) (BatchNorm, as cfg 3).
 * cfg 5 (Fixup ResNet-50): inputs come from the chain's own seeded forward
   pass (``chain.FixupChain``), not from here.
 
@@ -188,14 +189,24 @@ def _layer_seed(config: str, li: int, seed: int) -> list[int]:
 
 
 def spatial_activation(shape4, target: float, gen, device="cpu"):
-    """cfg 4: ReLU(conv3x3_rand(X) - tau), X ~ N(0,1), He-normal random C->C
-    weights, tau = the `target` quantile of the conv output (estimated from
-    1 M seeded samples).  torch on `device` (CPU for parity fixtures, CUDA in
-    the bench setup); returns a float32 tensor of `shape4`."""
+    """cfg 4: ReLU(conv3x3_rand(X) - tau), X ~ N(0,1), tau = the `target`
+    quantile of the conv output (estimated from 1 M seeded samples).
+
+    The random conv's weights are w[co, ci] = a[co, ci] * B + e[co, ci] with
+    a ~ N(0, 1/C), B the 3x3 binomial (smoothing) kernel and a small He-normal
+    part e: every output channel is a random mix of smoothed input channels,
+    so neighbouring pixels correlate (~0.6 at lag 1) and the ReLU zeros come
+    in spatial clusters, as in real feature maps.  (Purely zero-mean He-normal
+    weights would leave neighbours uncorrelated in expectation.)  torch on
+    `device` (CPU for parity fixtures, CUDA in the bench setup)."""
     import torch
     import torch.nn.functional as F
     N, C, H, W = shape4
-    w = torch.randn((C, C, 3, 3), generator=gen, device=device, dtype=torch.float32) * float(np.sqrt(2.0 / (9 * C)))
+    b1 = torch.tensor([1.0, 2.0, 1.0], device=device)
+    blur = torch.outer(b1, b1) / 16.0
+    a = torch.randn((C, C, 1, 1), generator=gen, device=device, dtype=torch.float32) / float(np.sqrt(C))
+    e = torch.randn((C, C, 3, 3), generator=gen, device=device, dtype=torch.float32) * float(0.25 / np.sqrt(9 * C))
+    w = a * blur + e
     out = torch.empty(shape4, device=device, dtype=torch.float32)
     step = max(1, (1 << 26) // max(1, C * H * W))  # bound the conv's temporary
     for i in range(0, N, step):
