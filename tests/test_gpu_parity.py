@@ -668,3 +668,4 @@ def test_vector_probes_match_reference_semantics(sp):  # test_vec.cpp:38-57, ker
             fused = (a.astype(np.float64) + np.float64(s) * w.astype(np.float64)).astype(np.float32)
             assert np.array_equal(p.broadcast_fma(a, s, w), fused)
             assert np.array_equal(p.add(a, w), (a + w).astype(np.float32))
+
