@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SPC_ABI_VERSION 1
+#define SPC_ABI_VERSION 2 /* 2: spc_epilogue.beta, multi-GPU comm entries, spc_vector_probe */
 
 typedef enum {
     SPC_OK = 0,

@@ -128,7 +128,7 @@ def load():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        if L.spc_abi_version() != 1:
+        if L.spc_abi_version() != 2:
             raise ImportError("libspconv_b200.so ABI version mismatch")
         _lib = L
     return _lib
