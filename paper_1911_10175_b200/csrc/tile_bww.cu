@@ -534,6 +534,11 @@ cudaError_t launch_tile_bww_variant(int variant, bool check_input, bool sparse, 
 
 bool tile_bww_supported(bool check_input, const DevShape& sh, int V) {
     if (V != 16) return false;
+    // the staging descriptors hold 32-bit element offsets (tile_bww_kernel
+    // cgo / ogo); larger tensors take the shape-general kernel (size_t)
+    const size_t chwnn = (size_t)((sh.N + 15) / 16) * 16 * sh.C * sh.H * sh.W;
+    const size_t dy = (size_t)((sh.N + 15) / 16) * 16 * sh.K * sh.Hp * sh.Wp;
+    if (chwnn >= (1ull << 32) || dy >= (1ull << 32)) return false;
     const int Lc = check_input ? sh.K : sh.C, Mc = check_input ? sh.C : sh.K;
     if (Lc % 64 || Mc % 16) return false;
     if (sh.R != sh.S || sh.O != sh.P) return false;
