@@ -87,3 +87,23 @@ def test_conv1_2_n32_deepest_bww_reduction_vs_64bit_oracle(sp, s, check):
     want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), 2, V, 30, check), D if check == 0 else dY)
     assert res.counters.executed_vector_fmas == want["executed_vector_fmas"]
     assert res.counters.checked_vectors == want["checked_vectors"]
+
+
+def test_vgg16_b32_dense_mode_matches_reference_dense_mode(sp):
+    """run_mode::dense (the reference's speedup denominator, P/include/spconv/
+    kernels.hpp:24): every layer x FWD / BWI / BWW (both checks) at the full
+    batch, against the reference's own dense-mode run_parallel; counters
+    equal its dense totals (checked_vectors = 0)."""
+    from paper_1911_10175_b200 import workloads as wl
+    worst = 0.0
+    for li, layer in enumerate(wl.vgg16(32)):
+        sh = layer.shape
+        D, G, dY = wl.layer_inputs_host("vgg16_b32", li, sh, 0.4, seed=1)
+        for comp, check, a, b in ((0, 0, D, G), (1, 0, dY, G), (2, 0, D, dY), (2, 1, D, dY)):
+            ctx = (layer.name, "dense", comp, check)
+            res = ref_vs_gpu(sp, sh, comp, check, a, b, mode=1)
+            assert res["finite"] and res["err"] <= TOL, (ctx, res["err"])
+            assert_counts_equal(res, ctx)
+            assert res["gpu"].checked_vectors == 0
+            worst = max(worst, res["err"])
+    print(f"dense mode: worst max|d|/max|ref| vs reference CPU {worst:.2e}")
