@@ -107,3 +107,23 @@ def test_vgg16_b32_dense_mode_matches_reference_dense_mode(sp):
             assert res["gpu"].checked_vectors == 0
             worst = max(worst, res["err"])
     print(f"dense mode: worst max|d|/max|ref| vs reference CPU {worst:.2e}")
+
+
+def test_vgg16_b32_tf32x3_variant_matches_reference(sp):
+    """The optional 3xTF32 tensor-core variant (DESIGN 4.7, stated tolerance
+    1e-5) through its production dispatch at the benched size: every layer x
+    FWD / BWI / BWW (both checks) at s = 0.6 vs the reference CPU, counters
+    exact."""
+    from paper_1911_10175_b200 import workloads as wl
+    worst = 0.0
+    with sp.math_mode(sp.Math.tf32x3):
+        for li, layer in enumerate(wl.vgg16(32)):
+            sh = layer.shape
+            D, G, dY = wl.layer_inputs_host("vgg16_b32", li, sh, 0.6, seed=2)
+            for comp, check, a, b in ((0, 0, D, G), (1, 0, dY, G), (2, 0, D, dY), (2, 1, D, dY)):
+                ctx = (layer.name, "tf32x3", comp, check)
+                res = ref_vs_gpu(sp, sh, comp, check, a, b)
+                assert res["finite"] and res["err"] <= TOL, (ctx, res["err"])
+                assert_counts_equal(res, ctx)
+                worst = max(worst, res["err"])
+    print(f"tf32x3: worst max|d|/max|ref| vs reference CPU {worst:.2e}")
