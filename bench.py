@@ -257,6 +257,28 @@ SPARSITY_NOTE = {
 
 
 # ---------------------------------------------------------------- our arm
+class TorchComm:
+    """The product communicator's interface (window / allreduce / close) over a
+    torch.distributed group -- only for SPC_BENCH_BACKEND=gloo dry runs."""
+
+    def __init__(self, dist):
+        self.dist = dist
+        self.size = dist.get_world_size()
+
+    def window(self, numel):
+        import torch
+        return torch.zeros(numel, dtype=torch.float32, device="cuda"), False
+
+    def allreduce(self, buf, stream_ptr):
+        import torch
+        st = torch.cuda.ExternalStream(stream_ptr)
+        st.synchronize()
+        self.dist.all_reduce(buf)
+
+    def close(self):
+        pass
+
+
 def relaunch_distributed(args) -> int:
     """`python bench.py --gpus N` outside torchrun: re-exec this script as N
     ranks under torch.distributed.run (one process per GPU, 127.0.0.1
@@ -342,14 +364,24 @@ def main():
     from paper_1911_10175_b200.dist import Comm, shard_range
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # SPC_BENCH_BACKEND=gloo: a dry run of the multi-rank logic (sharding,
+    # max-over-ranks timing, the JSON line) with several ranks on ONE GPU --
+    # NCCL refuses two ranks per device; the dG exchange then goes through
+    # torch.distributed (gloo) instead of the product communicator.  Numbers
+    # from such a run are not measurements.
+    dry_backend = os.environ.get("SPC_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     # under torchrun (any world size) the collective path is live: the
     # product's NCCL communicator (csrc/comm.cu) with dG in a symmetric window,
     # per-layer allreduce on a comm stream, barriers, max-over-ranks timing
     distributed = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
     comm = None
-    if distributed:
+    if distributed and dry_backend == "gloo":
+        dist.init_process_group("gloo")
+        comm = TorchComm(dist)
+        log(f"[rank {rank}] dry run: gloo process group, {ws} ranks on cuda:{dev.index}")
+    elif distributed:
         dist.init_process_group("nccl", device_id=dev)
         comm = Comm()
         log(f"[rank {rank}] spc_comm: {comm.size} ranks, NCCL {sp._lib.load().spc_nccl_version()}")
@@ -493,7 +525,9 @@ def main():
         "clocks": clocks.summary(), "roofline": roofline, "sweep": breakdown,
         "dense_mode_at_s0": dense0,
     }
-    if comm is not None:
+    if comm is not None and dry_backend == "gloo":
+        out["collective"] = {"impl": "DRY RUN: torch.distributed gloo, several ranks on one GPU -- not a measurement"}
+    elif comm is not None:
         out["collective"] = {"impl": "spc_bww_allreduce (csrc/comm.cu) on a comm stream",
                              "nccl_version": sp._lib.load().spc_nccl_version(), "ranks": comm.size,
                              "dG_symmetric_window": symmetric, "dG_bytes_per_step": 4 * dg_total}
