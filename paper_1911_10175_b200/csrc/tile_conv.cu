@@ -709,14 +709,16 @@ __global__ void __launch_bounds__(256) density_probe_kernel(const float* __restr
     const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     const size_t stride = n4 / (nthreads * 16) > 0 ? n4 / (nthreads * 16) : 1;
     unsigned nz = 0, tot = 0;
+    // all 16 loads in flight at once (one DRAM round trip, not 16)
+    float4 v[16];
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
         const size_t e = (tid + (size_t)i * nthreads) * stride;
-        if (e < n4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(t) + e);
-            nz += (v.x != 0.0f) + (v.y != 0.0f) + (v.z != 0.0f) + (v.w != 0.0f);
-            tot += 4;
-        }
+        v[i] = e < n4 ? __ldg(reinterpret_cast<const float4*>(t) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        tot += e < n4 ? 4u : 0u;
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) nz += (v[i].x != 0.0f) + (v[i].y != 0.0f) + (v[i].z != 0.0f) + (v[i].w != 0.0f);
     nz = __reduce_add_sync(0xffffffffu, nz);
     tot = __reduce_add_sync(0xffffffffu, tot);
     if ((threadIdx.x & 31) == 0) {
