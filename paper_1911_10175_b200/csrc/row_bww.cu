@@ -423,18 +423,12 @@ static cudaError_t launch_row_cfg(bool sparse, const DevShape& sh, const float* 
 }
 
 // The row kernel for a finite D (sel = 1); the caller enqueues the exact
-// kernel for sel = 0.  SPC_ROW_CFG selects a tuning variant (development).
+// kernel for sel = 0.  KK=4 (128 lane channels) only runs when forced
+// (SPC_ROW_BWW=1): it measured slower than the tile kernel;
+// variants of round 2's sweep (shuffled values instead of the preloaded row,
+// CB = 2, KK = 2 on 128-channel layers) were slower still and are not built.
 cudaError_t launch_row_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
                                 unsigned long long* exec_ctr, const int* sel, cudaStream_t st) {
-    static const int cfg = std::getenv("SPC_ROW_CFG") ? std::atoi(std::getenv("SPC_ROW_CFG")) : 0;
-    if (sh.K % 128 == 0) {
-        switch (cfg) {
-        case 1: return launch_row_cfg<4, 4, 4, 4, false>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
-        case 3: return launch_row_cfg<2, 4, 4, 4, true>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
-        case 4: return launch_row_cfg<4, 2, 4, 4, true>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
-        default: break;
-        }
-    }
     if (sh.K % 128 == 0)
         return launch_row_cfg<4, 4, 4, 4, true>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
     return launch_row_cfg<2, 4, 4, 4, true>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
