@@ -21,9 +21,10 @@
 //   * Per input row the warp loads its CB x (TW+2) checked values with one
 //     conflict-free LDS per lane, takes ONE __ballot_sync (the nonzero mask of
 //     the whole row for all its channels, the paper's per-vector zero check),
-//     and then visits only the set bits: ffs, shfl of the value from the lane
-//     that loaded it, and a jump-table switch into a block of static-register
-//     FFMA2s (acc[c][tap] += d * dY[tap's output pixel]).  Zeros cost nothing.
+//     and walks the bits with one warp-uniform branch each into a block of
+//     static-register FFMA2s (acc[c][tap] += d * dY[tap's output pixel]); a
+//     zero costs its branch only.  (Dispatching set bits through a jump table
+//     -- brx per nonzero -- measured 4-6x slower.)
 //   * Rows are staged by a cp.async pipeline (NST rows deep, one barrier per
 //     row): the dY row as 16-byte copies of the ActNCHWc channel vectors, the
 //     checked row's (TW+2) pixels per channel out of ActCHWNn.
@@ -36,7 +37,6 @@
 //     (popcount x valid targets x K/V), per lane from the row's mask.
 //   * The reduction over (image, strip) items is split over CTAs in fixed
 //     item ranges; the partials are summed in fixed order (deterministic).
-#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -107,18 +107,9 @@ __device__ __forceinline__ void row_bits_pre(uint32_t m, const float (&dv)[CB * 
     }
 }
 
-template <int KK, int CB, int TW, int PH, int J>
-__device__ __forceinline__ void row_bits(uint32_t m, float val, float2 (&acc)[CB][9][KK / 2],
-                                         const float2 (&win)[3][TW][KK / 2]) {
-    if constexpr (J < CB * (TW + 2)) {
-        if (m & (1u << J)) row_block<KK, CB, TW, PH, J>(acc, win, __shfl_sync(0xffffffffu, val, J));
-        row_bits<KK, CB, TW, PH, J + 1>(m, val, acc, win);
-    }
-}
-
 }  // namespace
 
-template <int KK, int CB, int NW, int TW, bool SPARSE, bool PRE>
+template <int KK, int CB, int NW, int TW, bool SPARSE>
 __global__ void __launch_bounds__(NW * 32) row_bww_kernel(DevShape sh, const float* __restrict__ chk,
                                                           const float* __restrict__ oth,
                                                           float* __restrict__ partial, int splits,
@@ -258,8 +249,7 @@ __global__ void __launch_bounds__(NW * 32) row_bww_kernel(DevShape sh, const flo
             }
         }
         if (s == 0) return;
-        // 2. checked row y = s - 1: one ballot for the warp's CB channels x RW
-        //    pixels; a set bit's value comes from the lane that loaded it
+        // 2. checked row y = s - 1: one ballot for the warp's CB channels x RW pixels
         const int y = s - 1;
         const float* drow = base + warp * CB * G::DROW;
         const float val = lane < NB ? drow[lcc * G::DROW + lr] : 0.0f;
@@ -269,23 +259,20 @@ __global__ void __launch_bounds__(NW * 32) row_bww_kernel(DevShape sh, const flo
         cnt += nz ? (uint32_t)(rv * cv) : 0u;
         const uint32_t m = __ballot_sync(0xffffffffu, nz);
         if (m == 0) return;
-        if constexpr (PRE) {
-            // the row's values as broadcast 128-bit loads, all issued before the first FMA
-            float dv[NB];
+        // the row's values as broadcast 128-bit loads, all issued before the first FMA
+        // (measured faster than fetching each set bit's value with a shuffle)
+        float dv[NB];
 #pragma unroll
-            for (int a = 0; a < CB; ++a)
+        for (int a = 0; a < CB; ++a)
 #pragma unroll
-                for (int h = 0; h < (RW + 3) / 4; ++h) {
-                    const float4 q = *reinterpret_cast<const float4*>(drow + a * G::DROW + 4 * h);
-                    const float e4[4] = {q.x, q.y, q.z, q.w};
+            for (int h = 0; h < (RW + 3) / 4; ++h) {
+                const float4 q = *reinterpret_cast<const float4*>(drow + a * G::DROW + 4 * h);
+                const float e4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-                    for (int z = 0; z < 4; ++z)
-                        if (4 * h + z < RW) dv[a * RW + 4 * h + z] = e4[z];
-                }
-            row_bits_pre<KK, CB, TW, PH, 0>(m, dv, acc, win);
-        } else {
-            row_bits<KK, CB, TW, PH, 0>(m, val, acc, win);
-        }
+                for (int z = 0; z < 4; ++z)
+                    if (4 * h + z < RW) dv[a * RW + 4 * h + z] = e4[z];
+            }
+        row_bits_pre<KK, CB, TW, PH, 0>(m, dv, acc, win);
     };
 
     // consumer cursor (item, stage) advanced incrementally: no divisions per row
@@ -369,7 +356,7 @@ bool row_bww_supported(bool check_input, const DevShape& sh, int V) {
 }
 
 
-template <int KK, int CB, int NW, int TW, bool PRE>
+template <int KK, int CB, int NW, int TW>
 static cudaError_t launch_row_cfg(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
                                   unsigned long long* exec_ctr, const int* sel, cudaStream_t st) {
     using G = RowGeom<KK, CB, NW, TW>;
@@ -378,7 +365,7 @@ static cudaError_t launch_row_cfg(bool sparse, const DevShape& sh, const float* 
     if ((size_t)((sh.N + 15) / 16) * 16 * sh.C * sh.H * sh.W >= (1ull << 32) ||
         (size_t)sh.N * sh.K * sh.Hp * sh.Wp >= (1ull << 32))
         return cudaErrorInvalidValue;
-    auto kern = sparse ? row_bww_kernel<KK, CB, NW, TW, true, PRE> : row_bww_kernel<KK, CB, NW, TW, false, PRE>;
+    auto kern = sparse ? row_bww_kernel<KK, CB, NW, TW, true> : row_bww_kernel<KK, CB, NW, TW, false>;
     static PerDeviceOnce attr[2];
     int ad = 0;
     if (attr[sparse].needed(ad)) {
@@ -430,8 +417,8 @@ static cudaError_t launch_row_cfg(bool sparse, const DevShape& sh, const float* 
 cudaError_t launch_row_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
                                 unsigned long long* exec_ctr, const int* sel, cudaStream_t st) {
     if (sh.K % 128 == 0)
-        return launch_row_cfg<4, 4, 4, 4, true>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
-    return launch_row_cfg<2, 4, 4, 4, true>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
+        return launch_row_cfg<4, 4, 4, 4>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
+    return launch_row_cfg<2, 4, 4, 4>(sparse, sh, chk, oth, dst, exec_ctr, sel, st);
 }
 
 }  // namespace spc
