@@ -109,15 +109,23 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
     static const int row_env = std::getenv("SPC_ROW_BWW") ? std::atoi(std::getenv("SPC_ROW_BWW")) : -1;
     const bool row_pick = row_env == 1 || (row_env == -1 && sh.K % 128 != 0);
     const bool use_row = !force_generic && row_pick && row_bww_supported(check_input, sh, V);
-    if (use_row || (!force_generic && tile_bww_supported(check_input, sh, V))) {
+    // 3x3 s1 check=input with 128-multiple lane blocks: the TMA-staged tile kernel
+    // (tma_bww.cu), 7-10% faster than the cp.async tile kernel at every sparsity
+    // of the VGG sweep.  SPC_TMA_BWW=0 keeps the cp.async kernel (A/B); =2 (DEV
+    // build) also takes the 64-channel layers from the row kernel.
+    static const int tma_env = std::getenv("SPC_TMA_BWW") ? std::atoi(std::getenv("SPC_TMA_BWW")) : 1;
+    const bool use_tma = !force_generic && (!use_row || tma_env == 2) && tma_env >= 1 && row_env != 1 &&
+                         tma_bww_supported(check_input, sh, V);
+    if (use_row || use_tma || (!force_generic && tile_bww_supported(check_input, sh, V))) {
         const size_t chk_n = (size_t)((sh.N + 15) / 16) * 16 *
                              (check_input ? (size_t)sh.C * sh.H * sh.W : (size_t)sh.K * sh.Hp * sh.Wp);
         int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
         cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
         launch_finite_all(chk, chk_n, finite, st);
-        e = use_row ? launch_row_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, st)
-                    : launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, finite, 1);
+        e = use_row && !use_tma ? launch_row_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, st)
+            : use_tma ? launch_tma_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, 1, st)
+                      : launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, finite, 1);
         if (e == cudaSuccess) {
             const int gs = bww_generic_splits(sh);
             const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;

@@ -20,4 +20,10 @@ bool row_bww_supported(bool check_input, const DevShape& sh, int V);
 cudaError_t launch_row_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
                                 unsigned long long* exec_ctr, const int* sel, cudaStream_t st);
 
+// tma_bww.cu: check = input, 3x3 stride 1 pad 1, K % 128 == 0 (TMA-staged tile kernel)
+bool tma_bww_supported(bool check_input, const DevShape& sh, int V);
+// runs when *sel == want (sel == nullptr: always)
+cudaError_t launch_tma_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
+                                unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st);
+
 }  // namespace spc

@@ -652,6 +652,82 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
 
+def test_tma_bww_kernel_matches_oracle(sp):
+    """The TMA-staged BWW tile kernel (csrc/tma_bww.cu; the default for
+    check=input 3x3 s1 with K % 128 == 0): ragged image blocks (N % 16 != 0),
+    widths that are not tile multiples (overhanging tiles, plane pitch > W + 1),
+    one-tile images, sparse and dense mode, exact counters, run-to-run bitwise."""
+    V = 16
+    for (n, C, K, H, W) in [(3, 16, 128, 9, 10), (17, 32, 128, 14, 13), (2, 16, 256, 7, 30), (1, 48, 128, 5, 5),
+                            (33, 16, 128, 3, 4), (2, 16, 128, 28, 28)]:
+        sh = sp.ConvShape.make(n, C, K, H, W, 3, 3, 1, 1)
+        for s in (0.0, 0.5, 0.9):
+            D = O.gen_sparse(n, C, H, W, s, n + C)
+            dY = O.gen_sparse(n, K, H, W, 0.0, K + W)
+            ref = O.dense(2, sh.astuple(), D, dY)
+            want = O.expected_counts(sh.astuple(), O.plan(sh.astuple(), 2, V), D)
+            pl = sp.plan(sh, sp.Component.bww, V)
+            a, b = sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda")
+            for mode in (0, 1):
+                res = sp.run_parallel(a, b, sh, pl, sp.RunMode(mode))
+                got = sp.unpack(res.out).cpu().numpy()
+                assert O.max_abs_rel(got, ref) <= TOL, (sh, s, mode)
+                assert res.counters.executed_vector_fmas == (want["executed_vector_fmas"] if mode == 0
+                                                             else want["dense_total"]), (sh, s, mode)
+                again = sp.run_parallel(a, b, sh, pl, sp.RunMode(mode))
+                assert np.array_equal(sp.unpack(again.out).cpu().numpy(), got)
+
+
+def test_tma_bww_nonfinite_input_takes_the_exact_fallback(sp):
+    """Inf/NaN in D at image corners and edges: the TMA kernel (which adds
+    d * 0 for partner pixels outside the image) must not run; the exact
+    shape-general kernel does, and the result equals the oracle's."""
+    V = 16
+    sh = sp.ConvShape.make(2, 16, 128, 9, 10, 3, 3, 1, 1)
+    D = O.gen_sparse(2, 16, 9, 10, 0.5, 5)
+    dY = O.gen_sparse(2, 128, 9, 10, 0.0, 6)
+    D[0, 0, 0, 0] = np.inf
+    D[1, 3, 8, 9] = np.nan
+    D[1, 5, 4, 0] = -np.inf
+    ref = O.dense(2, sh.astuple(), D, dY)
+    pl = sp.plan(sh, sp.Component.bww, V)
+    res = sp.run_parallel(sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pl,
+                          sp.RunMode.sparse)
+    got = sp.unpack(res.out).cpu().numpy()
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    assert np.array_equal(np.isinf(got), np.isinf(ref))
+    fin = np.isfinite(ref)
+    assert O.max_abs_rel(np.where(fin, got, 0), np.where(fin, ref, 0)) <= TOL
+
+
+def test_tma_bww_equals_cp_async_tile_kernel(tmp_path):
+    """A/B: SPC_TMA_BWW=0 (the cp.async tile kernel of tile_bww.cu) against the
+    default TMA kernel on one shape -- same counters, values within the bar."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, oracle as O, paper_1911_10175_b200 as sp
+V = 16
+sh = sp.ConvShape.make(18, 32, 128, 14, 14, 3, 3, 1, 1)
+D = O.gen_sparse(18, 32, 14, 14, 0.6, 1)
+dY = O.gen_sparse(18, 128, 14, 14, 0.0, 2)
+pl = sp.plan(sh, sp.Component.bww, V)
+res = sp.run_parallel(sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda"), sh, pl, sp.RunMode.sparse)
+np.save(sys.argv[1], sp.unpack(res.out).cpu().numpy())
+print("ok", res.counters.executed_vector_fmas)
+'''
+    outs = []
+    for knob in ("1", "0"):
+        env = dict(os.environ, SPC_TMA_BWW=knob)
+        f = str(tmp_path / f"dg{knob}.npy")
+        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=300,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+        outs.append((np.load(f), r.stdout.split()[-1]))
+    assert outs[0][1] == outs[1][1]
+    assert O.max_abs_rel(outs[0][0], outs[1][0]) <= TOL
+
+
 def test_vector_probes_match_reference_semantics(sp):  # test_vec.cpp:38-57, kernels.hpp:90-98
     rng = np.random.default_rng(8)
     for V in (4, 8, 16):
