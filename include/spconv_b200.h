@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SPC_ABI_VERSION 2 /* 2: spc_epilogue.beta, multi-GPU comm entries, spc_vector_probe */
+#define SPC_ABI_VERSION 3 /* 2: spc_epilogue.beta, multi-GPU comm entries, spc_vector_probe; 3: spc_run_parallel_host_batch */
 
 typedef enum {
     SPC_OK = 0,
@@ -181,6 +181,27 @@ int spc_get_math(void);
 /* ---- host-buffer drop-ins: copy in, run, copy out, synchronize ---- */
 spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const spc_shape* shape,
                                  const spc_plan* plan, int mode, spc_tensor* dst, spc_counters* counters);
+
+/* A list of host-buffer passes, run as if spc_run_parallel_host were called on
+ * each in order (the reference's bench loop over layers and components,
+ * P/src/bench.cpp:216-288, in one call) but pipelined across passes: pass
+ * i + 1's H2D overlaps pass i's kernels and D2H.  Results, counters and error
+ * behaviour per pass are those of spc_run_parallel_host; every pass is
+ * validated before any device work starts.  Pinned host buffers are pipelined;
+ * a pass with pageable buffers runs through spc_run_parallel_host at its turn.
+ * All buffers must stay valid until the call returns.  Returns the first
+ * failing pass's status (also in its `status`), SPC_OK otherwise. */
+typedef struct {
+    const spc_tensor* a;
+    const spc_tensor* b;
+    const spc_shape* shape;
+    const spc_plan* plan;
+    int mode;               /* spc_run_mode */
+    spc_tensor* dst;        /* data + capacity in, header out */
+    spc_counters* counters; /* may be NULL */
+    spc_status status;      /* out */
+} spc_host_pass;
+spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n);
 
 /* ---- ReLU semantics on device (P/src/sparsity.cpp:11-28), bit-exact ---- */
 spc_status spc_relu(const float* in, float* out, size_t n, void* stream);

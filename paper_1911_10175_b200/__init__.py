@@ -9,7 +9,7 @@ harness's timed sweeps and CSVs; :mod:`.chain` layer chains (ResNet-50 /
 Fixup) with fused ReLU epilogues.
 """
 from .api import (BackendPref, BlockedTensor, BwwCheck, Component, ConvResult, ConvShape, Epilogue,  # noqa: F401
-                  KernelCounters, KernelPlan, Math, get_math, math_mode, set_math, epilogue_apply, Layout, PreparedPass, RunMode, SpconvError, analytic_counters, backend_name,
+                  HostBatch, KernelCounters, KernelPlan, Math, get_math, math_mode, set_math, epilogue_apply, Layout, PreparedPass, RunMode, SpconvError, analytic_counters, backend_name,
                   backend_names, launch_count, native_backend_available, nchwc_to_chwnn, output_shape,
                   VecProbe, vector_probes,
                   pack_act_chwnn, pack_act_nchwc, pack_filter, plan, relu_, relu_grad_mask, run_parallel,

@@ -43,6 +43,12 @@ class spc_tensor(C.Structure):
                 ("data", C.c_void_p), ("numel", C.c_size_t)]
 
 
+class spc_host_pass(C.Structure):
+    _fields_ = [("a", C.POINTER(spc_tensor)), ("b", C.POINTER(spc_tensor)), ("shape", C.POINTER(spc_shape)),
+                ("plan", C.POINTER(spc_plan)), ("mode", C.c_int), ("dst", C.POINTER(spc_tensor)),
+                ("counters", C.POINTER(spc_counters)), ("status", C.c_int)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "spc_abi_version": (C.c_int, []),
@@ -77,6 +83,7 @@ _SIGS = {
     "spc_run_parallel_host": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.POINTER(spc_shape),
                                         C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor),
                                         C.POINTER(spc_counters)]),
+    "spc_run_parallel_host_batch": (C.c_int, [C.POINTER(spc_host_pass), C.c_int]),
     "spc_relu": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_relu_grad_mask": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_nchwc_to_chwnn": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.c_void_p]),
@@ -128,7 +135,7 @@ def load():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        if L.spc_abi_version() != 2:
+        if L.spc_abi_version() != 3:
             raise ImportError("libspconv_b200.so ABI version mismatch")
         _lib = L
     return _lib

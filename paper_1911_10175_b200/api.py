@@ -569,6 +569,59 @@ def run_parallel(a: BlockedTensor, b: BlockedTensor, shape: ConvShape, pl: Kerne
     return _run(Component(pl.comp), a, b, shape, pl, mode, workers, pref)
 
 
+class HostBatch:
+    """A prepared list of host-buffer passes for ``spc_run_parallel_host_batch``
+    (include/spconv_b200.h): the reference's bench loop over layers and
+    components (P/src/bench.cpp:216-288) as one call whose H2D copies, kernels
+    and D2H copies are pipelined across passes.  ``add`` takes host (numpy)
+    operands and an optional preallocated output; ``run`` executes every pass
+    and returns one ConvResult per pass (counters included).  Buffers in
+    pinned memory are pipelined; pageable ones go through the per-call path."""
+
+    def __init__(self):
+        self._keep = []
+        self._items = []
+
+    def add(self, a: BlockedTensor, b: BlockedTensor, shape: ConvShape, pl: KernelPlan,
+            mode: RunMode = RunMode.sparse, out=None) -> int:
+        if a.on_device or b.on_device:
+            raise SpconvError(_lib.SPC_ERR_ARG, "HostBatch takes host operands")
+        desc, numel = output_desc(shape, pl)
+        o = out if out is not None else np.empty(numel, np.float32)
+        item = dict(ca=a.to_c(), cb=b.to_c(), cs=shape.to_c(), cp=pl.to_c(), mode=int(mode),
+                    cd=spc_tensor(0, 0, 0, 0, 0, 0, 0, 0, 0, o.ctypes.data, o.size), cnt=spc_counters(),
+                    out=o, desc=desc)
+        self._keep.append((a, b))
+        self._items.append(item)
+        return len(self._items) - 1
+
+    def __len__(self):
+        return len(self._items)
+
+    def run(self):
+        L = _lib.load()
+        n = len(self._items)
+        arr = (_lib.spc_host_pass * n)()
+        for i, it in enumerate(self._items):
+            it["cd"].data = it["out"].ctypes.data
+            it["cd"].numel = it["out"].size
+            arr[i].a = C.pointer(it["ca"])
+            arr[i].b = C.pointer(it["cb"])
+            arr[i].shape = C.pointer(it["cs"])
+            arr[i].plan = C.pointer(it["cp"])
+            arr[i].mode = it["mode"]
+            arr[i].dst = C.pointer(it["cd"])
+            arr[i].counters = C.pointer(it["cnt"])
+            arr[i].status = 0
+        _check(L.spc_run_parallel_host_batch(arr, n))
+        res = []
+        for it in self._items:
+            d = dataclasses.replace(it["desc"]) if dataclasses.is_dataclass(it["desc"]) else it["desc"]
+            d.data = it["out"]
+            res.append(ConvResult(d, KernelCounters._from_c(it["cnt"]), L.spc_backend_name().decode()))
+        return res
+
+
 class PreparedPass:
     """A validated, device-resident pass with a preallocated output, for
     repeated asynchronous launches (bench / training loops).  ``launch`` does
@@ -589,6 +642,7 @@ class PreparedPass:
         self._ca, self._cb = a.to_c(), b.to_c()
         self._cd = spc_tensor(0, 0, 0, 0, 0, 0, 0, 0, 0, self.out.data_ptr(), numel)
         self._shape, self._plan = shape.to_c(), pl.to_c()
+        self.shape_obj, self.plan_obj = shape, pl
         self._mode = int(mode)
         if epilogue is not None and Component(pl.comp) == Component.bww:
             raise SpconvError(_lib.SPC_ERR_ARG, "BWW has no output epilogue")

@@ -1062,6 +1062,294 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     return SPC_OK;
 }
 
+// ---------------------------------------------------------------- host-buffer batch
+// spc_run_parallel_host_batch: a list of host-buffer passes run as if
+// spc_run_parallel_host were called on each in order, but pipelined ACROSS
+// passes: pass i+1's H2D starts while pass i's kernels and D2H are still in
+// flight, so the two copy engines and the SMs stay busy for the whole list
+// instead of draining at every call (the per-call form exposes each call's
+// first H2D chunk and last kernel + D2H chunk).  Up to batch_slots() passes are
+// in flight, each in its own slice of a per-thread device arena (no
+// allocation inside the pipeline); every copy runs on the copy-in / copy-out
+// streams of the per-call path, every kernel on its compute stream.
+namespace {
+constexpr int kBatchSlotsMax = 8;
+static int batch_slots() {
+    static const int v = std::getenv("SPC_BATCH_SLOTS") ? std::atoi(std::getenv("SPC_BATCH_SLOTS")) : 3;
+    return v < 1 ? 1 : v > kBatchSlotsMax ? kBatchSlotsMax : v;
+}
+constexpr int kBatchChunks = 16;
+struct BatchSlot {
+    cudaEvent_t in_done[kBatchChunks] = {};
+    cudaEvent_t k_done[kBatchChunks] = {};
+    cudaEvent_t done = nullptr;
+    spc_counters* hc = nullptr;  // pinned [kBatchChunks]
+    char* mem = nullptr;         // this slot's slice of the arena
+    // the pass in flight
+    int pass = -1, nc = 0;
+    spc_tensor out{};
+};
+struct BatchState {
+    int dev = -1;
+    char* arena = nullptr;
+    size_t slot_bytes = 0;
+    BatchSlot slot[kBatchSlotsMax];
+};
+thread_local BatchState g_bs;
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// device bytes one pass needs in its slot
+size_t batch_need(const spc_host_pass& p, const spc_tensor& out, int nc) {
+    const bool bww = p.plan->comp == SPC_BWW;
+    size_t n = align256(p.a->numel * sizeof(float)) + align256(p.b->numel * sizeof(float)) +
+               align256(out.numel * sizeof(float)) + align256(kBatchChunks * sizeof(spc_counters));
+    if (bww && nc > 1) n += align256((size_t)nc * out.numel * sizeof(float));
+    return n;
+}
+
+int batch_chunks(const spc_host_pass& p, const spc_tensor& out) {
+    static const int chunk_mb = std::getenv("SPC_BATCH_CHUNK_MB") ? std::atoi(std::getenv("SPC_BATCH_CHUNK_MB")) : 128;
+    const bool bww = p.plan->comp == SPC_BWW;
+    const int units = bww ? (p.shape->N + p.plan->V - 1) / p.plan->V : p.shape->N;
+    const size_t io = (p.a->numel + p.b->numel + out.numel) * sizeof(float);
+    int nc = (int)((io + ((size_t)chunk_mb << 20) - 1) / ((size_t)chunk_mb << 20));
+    if (nc > kBatchChunks) nc = kBatchChunks;
+    if (nc > units) nc = units;
+    return nc < 1 ? 1 : nc;
+}
+
+spc_status batch_state(BatchState*& bs, size_t slot_bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e;
+    if (g_bs.dev != dev) {
+        for (auto& sl : g_bs.slot) {
+            for (int c = 0; c < kBatchChunks; ++c)
+                if ((e = cudaEventCreateWithFlags(&sl.in_done[c], cudaEventDisableTiming)) != cudaSuccess ||
+                    (e = cudaEventCreateWithFlags(&sl.k_done[c], cudaEventDisableTiming)) != cudaSuccess)
+                    return cuda_fail(e, "event create");
+            if ((e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "event create");
+            if ((e = cudaMallocHost((void**)&sl.hc, kBatchChunks * sizeof(spc_counters))) != cudaSuccess)
+                return cuda_fail(e, "pinned alloc");
+        }
+        g_bs.arena = nullptr;
+        g_bs.slot_bytes = 0;
+        g_bs.dev = dev;
+    }
+    if (g_bs.slot_bytes < slot_bytes) {  // grow (idle: no pass is in flight between batches)
+        if (g_bs.arena) cudaFree(g_bs.arena);
+        g_bs.arena = nullptr;
+        g_bs.slot_bytes = 0;
+        if ((e = cudaMalloc((void**)&g_bs.arena, slot_bytes * batch_slots())) != cudaSuccess)
+            return cuda_fail(e, "batch arena");
+        g_bs.slot_bytes = slot_bytes;
+        for (int i = 0; i < batch_slots(); ++i) g_bs.slot[i].mem = g_bs.arena + (size_t)i * slot_bytes;
+    }
+    bs = &g_bs;
+    return SPC_OK;
+}
+
+// enqueue one pass (pinned host buffers) into `sl`; no host synchronisation
+spc_status batch_enqueue(BatchSlot& sl, int idx, const spc_host_pass& p, const spc_tensor& out, HostStreams* hs) {
+    cudaStream_t s0 = hs->s[0], sin = hs->s[1], sout = hs->s[2];
+    const spc_shape* shape = p.shape;
+    const spc_plan* plan = p.plan;
+    const bool bww = plan->comp == SPC_BWW;
+    const int V = plan->V;
+    const bool on_input = plan->check == SPC_CHECK_INPUT;
+    const spc_tensor *a = p.a, *b = p.b;
+    const spc_tensor* chk = bww ? (on_input ? a : b) : a;
+    const spc_tensor* oth = bww ? (on_input ? b : a) : nullptr;
+    const int units = bww ? (shape->N + V - 1) / V : shape->N;
+    const int nc = batch_chunks(p, out);
+    char* m = sl.mem;
+    float* da = reinterpret_cast<float*>(m);
+    m += align256(a->numel * sizeof(float));
+    float* db = reinterpret_cast<float*>(m);
+    m += align256(b->numel * sizeof(float));
+    float* dd = reinterpret_cast<float*>(m);
+    m += align256(out.numel * sizeof(float));
+    spc_counters* dc = reinterpret_cast<spc_counters*>(m);
+    m += align256(kBatchChunks * sizeof(spc_counters));
+    float* dpart = reinterpret_cast<float*>(m);
+    sl.pass = idx;
+    sl.nc = nc;
+    sl.out = out;
+    cudaError_t ce = cudaSuccess;
+    auto ck = [&](cudaError_t x) {
+        if (x != cudaSuccess && ce == cudaSuccess) ce = x;
+    };
+    spc_status st = SPC_OK;
+    if (!bww) ck(cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, sin));
+    const float* hchk = chk->data;
+    float* dchk = chk == a ? da : db;
+    const float* hoth = oth ? oth->data : nullptr;
+    float* doth = oth ? (oth == a ? da : db) : nullptr;
+    const size_t chk_unit = chk->numel / units;
+    const size_t oth_unit = oth ? oth->numel / shape->N : 0;
+    const size_t out_unit = bww ? 0 : out.numel / shape->N;
+    for (int c = 0; c < nc && st == SPC_OK && ce == cudaSuccess; ++c) {
+        const int u0 = (int)((long)units * c / nc), u1 = (int)((long)units * (c + 1) / nc);
+        const int i0 = bww ? u0 * V : u0;
+        const int i1 = bww ? (u1 * V < shape->N ? u1 * V : shape->N) : u1;
+        spc_shape shc = *shape;
+        shc.N = i1 - i0;
+        ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
+                           (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        if (oth)
+            ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
+                               (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        ck(cudaEventRecord(sl.in_done[c], sin));
+        ck(cudaStreamWaitEvent(s0, sl.in_done[c], 0));
+        spc_tensor tchk = *chk, toth, tb = *b, td = out;
+        tchk.data = dchk + (size_t)u0 * chk_unit;
+        tchk.n = shc.N;
+        tchk.numel = (size_t)(u1 - u0) * chk_unit;
+        if (oth) {
+            toth = *oth;
+            toth.data = doth + (size_t)i0 * oth_unit;
+            toth.n = shc.N;
+            toth.numel = (size_t)(i1 - i0) * oth_unit;
+        }
+        spc_counters* dcc = p.counters ? dc + c : nullptr;
+        if (bww) {
+            td.data = nc > 1 ? dpart + (size_t)c * out.numel : dd;
+            const spc_tensor* in_t = on_input ? &tchk : &toth;
+            const spc_tensor* dy_t = on_input ? &toth : &tchk;
+            st = spc_sparse_bww(in_t, dy_t, &shc, plan, p.mode, &td, dcc, s0);
+        } else {
+            tb.data = db;
+            td.data = dd + (size_t)i0 * out_unit;
+            td.numel = (size_t)(i1 - i0) * out_unit;
+            st = plan->comp == SPC_FWD ? spc_sparse_fwd(&tchk, &tb, &shc, plan, p.mode, &td, dcc, s0)
+                                       : spc_sparse_bwi(&tchk, &tb, &shc, plan, p.mode, &td, dcc, s0);
+            if (st == SPC_OK) {
+                ck(cudaEventRecord(sl.k_done[c], s0));
+                ck(cudaStreamWaitEvent(sout, sl.k_done[c], 0));
+                ck(cudaMemcpyAsync(out.data + (size_t)i0 * out_unit, td.data, td.numel * sizeof(float),
+                                   cudaMemcpyDeviceToHost, sout));
+            }
+        }
+    }
+    if (st == SPC_OK && ce == cudaSuccess && bww) {
+        if (nc > 1) {
+            sum_partials_kernel<<<grid_for(out.numel), 256, 0, s0>>>(dpart, nc, out.numel, dd);
+            note_launch();
+            ck(cudaGetLastError());
+        }
+        ck(cudaEventRecord(sl.k_done[nc - 1], s0));
+        ck(cudaStreamWaitEvent(sout, sl.k_done[nc - 1], 0));
+        ck(cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, sout));
+    }
+    if (st == SPC_OK && ce == cudaSuccess && p.counters)
+        ck(cudaMemcpyAsync(sl.hc, dc, nc * sizeof(spc_counters), cudaMemcpyDeviceToHost, sout));
+    ck(cudaEventRecord(sl.done, sout));
+    if (st) return st;
+    if (ce != cudaSuccess) return cuda_fail(ce, "host batch (copy / event)");
+    return SPC_OK;
+}
+
+// wait for the pass in `sl`, deliver its counters and output header
+spc_status batch_finish(BatchSlot& sl, spc_host_pass* passes) {
+    if (sl.pass < 0) return SPC_OK;
+    spc_host_pass& p = passes[sl.pass];
+    sl.pass = -1;
+    cudaError_t e = cudaEventSynchronize(sl.done);
+    if (e != cudaSuccess) return p.status = cuda_fail(e, "host batch");
+    if (p.counters) {
+        std::memset(p.counters, 0, sizeof(*p.counters));
+        for (int c = 0; c < sl.nc; ++c) {
+            p.counters->checked_vectors += sl.hc[c].checked_vectors;
+            p.counters->executed_vector_fmas += sl.hc[c].executed_vector_fmas;
+            p.counters->output_vector_loads += sl.hc[c].output_vector_loads;
+            p.counters->output_vector_stores += sl.hc[c].output_vector_stores;
+        }
+    }
+    *p.dst = sl.out;
+    return p.status = SPC_OK;
+}
+}  // namespace
+
+spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
+    NvtxRange r("spc_run_parallel_host_batch");
+    if (n < 0 || (n > 0 && !passes)) return fail(SPC_ERR_ARG, "null pass list");
+    if (n == 0) return SPC_OK;
+    // validate everything before any device work (like the per-call form)
+    std::vector<spc_tensor> outs(n);
+    std::vector<char> direct(n);
+    size_t slot_bytes = 0;
+    for (int i = 0; i < n; ++i) {
+        spc_host_pass& p = passes[i];
+        p.status = SPC_OK;
+        if (!p.a || !p.b || !p.shape || !p.plan || !p.dst) return p.status = fail(SPC_ERR_ARG, "null argument");
+        spc_status st;
+        switch (p.plan->comp) {
+        case SPC_FWD: st = validate_fwd(p.a, p.b, *p.shape, *p.plan); break;
+        case SPC_BWI: st = validate_bwi(p.a, p.b, *p.shape, *p.plan); break;
+        case SPC_BWW: st = validate_bww(p.a, p.b, *p.shape, *p.plan); break;
+        default: st = fail(SPC_ERR_PLAN, "run_parallel: bad component");
+        }
+        if (st) return p.status = st;
+        if (p.mode != SPC_SPARSE && p.mode != SPC_DENSE) return p.status = fail(SPC_ERR_ARG, "bad run mode");
+        outs[i] = *p.dst;
+        if ((st = prepare_dst(*p.shape, *p.plan, &outs[i]))) return p.status = st;
+        // pageable buffers take the per-call path (its pinned staging ring) at their turn
+        direct[i] = !(is_pageable(p.a->data) || is_pageable(p.b->data) || is_pageable(outs[i].data));
+        if (direct[i]) {
+            const size_t need = batch_need(p, outs[i], batch_chunks(p, outs[i]));
+            if (need > slot_bytes) slot_bytes = need;
+        }
+    }
+    spc_status st;
+    if ((st = check_device())) return st;
+    HostStreams* hs = nullptr;
+    if ((st = host_streams(hs))) return st;
+    BatchState* bs = nullptr;
+    if (slot_bytes && (st = batch_state(bs, slot_bytes))) return st;
+    spc_status first = SPC_OK;
+    auto drain = [&]() {
+        for (int k = 0; k < kBatchSlotsMax && bs; ++k) {
+            const spc_status f = batch_finish(bs->slot[k], passes);
+            if (f && !first) first = f;
+        }
+    };
+    const int kBatchSlots = batch_slots();
+    int next_slot = 0;
+    for (int i = 0; i < n && !first; ++i) {
+        spc_host_pass& p = passes[i];
+        if (!direct[i]) {
+            drain();
+            if (first) break;
+            p.status = spc_run_parallel_host(p.a, p.b, p.shape, p.plan, p.mode, p.dst, p.counters);
+            if (p.status) first = p.status;
+            continue;
+        }
+        BatchSlot& sl = bs->slot[next_slot];
+        next_slot = (next_slot + 1) % kBatchSlots;
+        st = batch_finish(sl, passes);  // the pass that used this slot kBatchSlots passes ago
+        if (st) {
+            first = st;
+            break;
+        }
+        st = batch_enqueue(sl, i, p, outs[i], hs);
+        if (st) {
+            p.status = st;
+            first = st;
+        }
+    }
+    // finish in submission order
+    for (int k = 0; k < kBatchSlots && bs; ++k) {
+        const spc_status f = batch_finish(bs->slot[(next_slot + k) % kBatchSlots], passes);
+        if (f && !first) first = f;
+    }
+    if (first) {
+        for (int c = 0; c < 3; ++c) cudaStreamSynchronize(hs->s[c]);
+    }
+    return first;
+}
+
 spc_status spc_relu(const float* in, float* out, size_t n, void* stream) {
     if ((!in || !out) && n) return fail(SPC_ERR_ARG, "null pointer");
     spc_status st = check_device();

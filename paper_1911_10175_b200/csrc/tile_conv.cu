@@ -364,6 +364,12 @@ __device__ __forceinline__ void tile_conv_body(DevShape sh, const float* __restr
         for (int j = 0; j < KA; ++j) acc[t][j] = AccT(0);
 
     constexpr int NST = Gm::NST;
+#ifndef SPC_CONV_CUNROLL
+#define SPC_CONV_CUNROLL 1
+#endif
+    // channel-loop unroll factor.  Measured with 2 (VGG16 b32): dense mode +4%, the sparse
+    // branch kernel -3%, the jump-table kernel 3-4x slower (instruction-cache misses)
+    constexpr int CUNROLL = SPC_CONV_CUNROLL;
     bool use_jt = JT >= 100 && !FORCE;  // JT in 1..99: decided per block below, starting with branches
 #pragma unroll
     for (int d = 0; d < NST - 1; ++d) {
@@ -383,7 +389,7 @@ __device__ __forceinline__ void tile_conv_body(DevShape sh, const float* __restr
             for (int f = 0; f < TAPS; ++f) g[f].load(fcb + f * 256);
         }
 
-#pragma unroll 1
+#pragma unroll CUNROLL
         for (int c = 0; c < 16; ++c) {
             const float* P = Ds + (cb % NST) * 16 * PLANE + c * PLANE;
             GV gn[GPF == 1 ? TAPS : 1];

@@ -237,6 +237,14 @@ __global__ void __launch_bounds__(NWC * 32, MINB)
         asm volatile("barrier.sync.aligned %0, 32;" ::"r"(warp + 1) : "memory");
 
         const float* base = reinterpret_cast<const float*>(smem + s * G::STAGE);
+#ifdef SPC_TMA_NOCOMP  // probe: the staging pipeline alone (results are wrong)
+        if (sh.N > 0) {
+            acc[0][0][0] += base[lane];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_bar(s));
+            continue;
+        }
+#endif
         float O[TH * TW][KK];
         const float* Ob = base + lane * KK;
 #pragma unroll
@@ -261,6 +269,11 @@ __global__ void __launch_bounds__(NWC * 32, MINB)
                     const bool nz = v != 0.0f;
                     cnt += nz ? wt[w] : 0u;
                     m[w] = __ballot_sync(0xffffffffu, nz);
+#if defined(TRY_MV1)
+                    asm volatile("mov.b32 %0, %0;" : "+r"(m[w]));
+#elif defined(TRY_MV2)
+                    m[w] = __shfl_sync(0xffffffffu, m[w], 0);
+#endif
                 }
             }
             // region rows as broadcast vector loads, one row ahead (16-byte vectors; 8-byte
@@ -367,6 +380,23 @@ cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* chk, const 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long target_ctas = env_ctas > 0 ? env_ctas : (base >= 16 && base <= 128) ? nsm * 18L : nsm * 6L;
     long splits = (target_ctas + base - 1) / base;
+    if (env_ctas <= 0) {
+        // wave quantisation: among the split counts within -25% / +10% of the target, take the
+        // one whose grid fills its last wave best (MINB CTAs per SM; conv3_2: 42 splits = 9.08
+        // waves -> 37 splits = 8.00 waves, measured 2-3% faster)
+        const long slots = (long)nsm * MINB;
+        long best = splits;
+        double best_eff = 0.0;
+        for (long s = splits * 3 / 4 > 0 ? splits * 3 / 4 : 1; s <= splits + splits / 10; ++s) {
+            const long g = base * s;
+            const double eff = (double)g / (double)(((g + slots - 1) / slots) * slots);
+            if (eff > best_eff + 1e-9) {
+                best_eff = eff;
+                best = s;
+            }
+        }
+        splits = best;
+    }
     if (splits > items) splits = items;
     const size_t E = (size_t)sh.C * 9 * sh.K;
     const long cap = (long)((256ull << 20) / (E * sizeof(float)));

@@ -80,6 +80,49 @@ conv_result run(component comp, const blocked_tensor& a, const blocked_tensor& b
 
 }  // namespace
 
+std::vector<conv_result> run_batch(const std::vector<pass_request>& passes) {
+    const size_t n = passes.size();
+    std::vector<conv_result> res(n);
+    std::vector<spc_shape> cs(n);
+    std::vector<spc_plan> cp(n);
+    std::vector<spc_tensor> ca(n), cb(n), cd(n);
+    std::vector<spc_counters> cnt(n);
+    std::vector<spc_host_pass> hp(n);
+    for (size_t i = 0; i < n; ++i) {
+        const pass_request& p = passes[i];
+        SPCONV_REQUIRE(p.a != nullptr && p.b != nullptr, "run_batch: null operand");
+        cs[i] = to_c(p.shape);
+        cp[i] = to_c(p.plan);
+        spc_tensor od;
+        std::memset(&od, 0, sizeof(od));
+        check(spc_output_desc(&cs[i], &cp[i], &od));
+        conv_result& r = res[i];
+        r.out.layout = od.layout == SPC_LAYOUT_FILTER_KCRS_BLK ? tensor_layout::filter_kcrs_blk
+                                                               : tensor_layout::act_nchwc;
+        r.out.V = od.V;
+        r.out.n = od.n; r.out.c = od.c; r.out.h = od.h; r.out.w = od.w;
+        r.out.k = od.k; r.out.r = od.r; r.out.s = od.s;
+        r.out.data.assign(od.numel, 0.0f);
+        ca[i] = to_c(*p.a);
+        cb[i] = to_c(*p.b);
+        cd[i] = od;
+        cd[i].data = r.out.data.data();
+        cd[i].numel = r.out.data.size();
+        std::memset(&cnt[i], 0, sizeof(spc_counters));
+        hp[i] = spc_host_pass{&ca[i], &cb[i], &cs[i], &cp[i], p.mode == run_mode::sparse ? SPC_SPARSE : SPC_DENSE,
+                              &cd[i], &cnt[i], SPC_OK};
+    }
+    check(spc_run_parallel_host_batch(hp.data(), (int)n));
+    for (size_t i = 0; i < n; ++i) {
+        res[i].counters.checked_vectors = cnt[i].checked_vectors;
+        res[i].counters.executed_vector_fmas = cnt[i].executed_vector_fmas;
+        res[i].counters.output_vector_loads = cnt[i].output_vector_loads;
+        res[i].counters.output_vector_stores = cnt[i].output_vector_stores;
+        res[i].backend = spc_backend_name();
+    }
+    return res;
+}
+
 kernel_plan plan(const conv_shape& shape, component comp, int V, int register_budget, bww_check chk) {
     const spc_shape cs = to_c(shape);
     spc_plan p;

@@ -42,4 +42,19 @@ conv_result run_parallel(const blocked_tensor& a, const blocked_tensor& b, const
                          const kernel_plan& plan, run_mode mode, int workers,
                          backend_pref pref = backend_pref::automatic);
 
+// A list of passes in one call (spc_run_parallel_host_batch): the reference's bench loop over
+// layers and components (P/src/bench.cpp:216-288) with the copies and kernels of consecutive
+// passes pipelined.  Same results, counters and errors per pass as run_parallel; every pass is
+// validated before any device work.  blocked_tensor keeps its data in a std::vector (pageable
+// memory), which the library moves through its pinned staging ring pass by pass; buffers
+// registered with cudaHostRegister are pipelined across passes.
+struct pass_request {
+    const blocked_tensor* a;
+    const blocked_tensor* b;
+    conv_shape shape;
+    kernel_plan plan;
+    run_mode mode = run_mode::sparse;
+};
+std::vector<conv_result> run_batch(const std::vector<pass_request>& passes);
+
 }  // namespace spconv::cuda

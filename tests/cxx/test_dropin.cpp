@@ -128,6 +128,29 @@ int main() {
                     compare(sh, comp, chk, 16, 0.6, 5, "tile");
                 }
         }
+    // run_batch: three passes in one call equal the reference and the per-call results
+    {
+        const auto sh = conv_shape::make(3, 64, 128, 13, 11, 3, 3, 1, 1);
+        std::vector<inputs> ins;
+        std::vector<cuda::pass_request> reqs;
+        std::vector<kernel_plan> pls;
+        for (component comp : {component::fwd, component::bwi, component::bww}) {
+            ins.push_back(make_inputs(sh, comp, bww_check::input, 0.6, 16, 77));
+            pls.push_back(cuda::plan(sh, comp, 16, 30, bww_check::input));
+        }
+        for (size_t i = 0; i < ins.size(); ++i)
+            reqs.push_back(cuda::pass_request{&ins[i].a, &ins[i].b, sh, pls[i], run_mode::sparse});
+        const std::vector<conv_result> got = cuda::run_batch(reqs);
+        CHECK(got.size() == 3, "run_batch size");
+        for (size_t i = 0; i < got.size(); ++i) {
+            const conv_result one = cuda::run_parallel(ins[i].a, ins[i].b, sh, pls[i], run_mode::sparse, 1);
+            const conv_result ref = run_parallel(ins[i].a, ins[i].b, sh, plan(sh, pls[i].comp, 16, 30, bww_check::input),
+                                                 run_mode::sparse, 4);
+            CHECK(got[i].out.data == one.out.data, "run_batch pass %zu differs from the per-call result", i);
+            CHECK(got[i].counters == ref.counters, "run_batch pass %zu counters", i);
+            CHECK(max_abs_rel(unpack(got[i].out), unpack(ref.out)) <= 1e-5, "run_batch pass %zu value", i);
+        }
+    }
     // single interior non-zero: exactly 36 vector FMAs (test_kernels.cpp:97-110)
     {
         const int V = 8;

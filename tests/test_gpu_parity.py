@@ -728,6 +728,60 @@ print("ok", res.counters.executed_vector_fmas)
     assert O.max_abs_rel(outs[0][0], outs[1][0]) <= TOL
 
 
+def test_host_batch_equals_per_call(sp):
+    """spc_run_parallel_host_batch: pinned and pageable passes mixed, FWD / BWI /
+    BWW (multi-chunk: N = 40 gives three 16-image blocks), more passes than
+    pipeline slots -- outputs and counters bitwise those of one
+    spc_run_parallel_host call per pass."""
+    import torch
+    V = 16
+    rng = np.random.default_rng(3)
+    hb = sp.HostBatch()
+    want = []
+    for i, (n, C, K, H, W) in enumerate([(40, 32, 128, 14, 14), (5, 16, 32, 9, 11), (40, 128, 128, 14, 14),
+                                          (18, 64, 64, 12, 12)]):
+        sh = sp.ConvShape.make(n, C, K, H, W, 3, 3, 1, 1)
+        D = O.gen_sparse(n, C, H, W, 0.6, 10 + i)
+        G = O.gen_sparse(K, C, 3, 3, 0.0, 20 + i)
+        dY = O.gen_sparse(n, K, H, W, 0.5, 30 + i)
+        ops = [(sp.Component.fwd, sp.pack_act_nchwc(D, V), sp.pack_filter(G, V)),
+               (sp.Component.bwi, sp.pack_act_nchwc(dY, V), sp.pack_filter(G, V, True)),
+               (sp.Component.bww, sp.pack_act_chwnn(D, V), sp.pack_act_nchwc(dY, V))]
+        for j, (comp, a, b) in enumerate(ops):
+            pl = sp.plan(sh, comp, V)
+            ref = sp.run_parallel(a, b, sh, pl, sp.RunMode.sparse)  # per-call host path (pageable numpy)
+            if (i + j) % 2 == 0:  # pinned operands and output: the pipelined path
+                a = sp.BlockedTensor(**{**a.header(), "data": torch.from_numpy(a.data).pin_memory().numpy()})
+                b = sp.BlockedTensor(**{**b.header(), "data": torch.from_numpy(b.data).pin_memory().numpy()})
+                out = torch.empty(ref.out.data.size, dtype=torch.float32).pin_memory().numpy()
+            else:
+                out = None
+            hb.add(a, b, sh, pl, sp.RunMode.sparse, out=out)
+            want.append(ref)
+    for rep in range(2):  # the second run reuses the arena and the slots
+        got = hb.run()
+        assert len(got) == len(want) == 12
+        for g, w in zip(got, want):
+            assert np.array_equal(g.out.data, w.out.data)
+            assert g.counters == w.counters
+            assert g.out.header() == w.out.header()
+
+
+def test_host_batch_validates_every_pass_before_device_work(sp):
+    V = 16
+    sh = sp.ConvShape.make(2, 16, 16, 5, 5, 3, 3, 1, 1)
+    D = O.gen_sparse(2, 16, 5, 5, 0.5, 1)
+    G = O.gen_sparse(16, 16, 3, 3, 0.0, 2)
+    pl = sp.plan(sh, sp.Component.fwd, V)
+    hb = sp.HostBatch()
+    hb.add(sp.pack_act_nchwc(D, V), sp.pack_filter(G, V), sh, pl)
+    hb.add(sp.pack_act_nchwc(D, V), sp.pack_filter(G, V), sh, pl, out=np.empty(7, np.float32))  # too small
+    n0 = sp.launch_count()
+    with pytest.raises(sp.SpconvError):
+        hb.run()
+    assert sp.launch_count() == n0
+
+
 def test_vector_probes_match_reference_semantics(sp):  # test_vec.cpp:38-57, kernels.hpp:90-98
     rng = np.random.default_rng(8)
     for V in (4, 8, 16):

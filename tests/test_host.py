@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(sp):
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(sp._lib.EXPORTED)
-    assert lib.spc_abi_version() == 2
+    assert lib.spc_abi_version() == 3
     dev = header_functions("spconv_b200_dev.h")
     assert set(dev) == set(sp._lib.DEV_EXPORTED)
     for n in dev:
