@@ -380,17 +380,20 @@ cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* chk, const 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long target_ctas = env_ctas > 0 ? env_ctas : (base >= 16 && base <= 128) ? nsm * 18L : nsm * 6L;
     long splits = (target_ctas + base - 1) / base;
-    if (env_ctas <= 0) {
-        // wave quantisation: among the split counts within -25% / +10% of the target, take the
-        // one whose grid fills its last wave best (MINB CTAs per SM; conv3_2: 42 splits = 9.08
-        // waves -> 37 splits = 8.00 waves, measured 2-3% faster)
+    static const bool wave_off = std::getenv("SPC_BWW_WAVE") && std::atoi(std::getenv("SPC_BWW_WAVE")) == 0;
+    if (env_ctas <= 0 && !wave_off && base <= 128) {
+        // wave quantisation (the many-wave shapes): among the split counts within -25% / +10%
+        // of the target, take the one whose grid fills its last wave best (MINB CTAs per SM;
+        // conv3_2: 42 splits = 9.08 waves -> 37 splits = 8.00 waves).  Measured 3-4% faster on
+        // VGG conv2_2 .. conv4_1; the few-wave shapes (base > 128) lose 8-10% with fewer
+        // splits and keep the plain target.
         const long slots = (long)nsm * MINB;
         long best = splits;
         double best_eff = 0.0;
         for (long s = splits * 3 / 4 > 0 ? splits * 3 / 4 : 1; s <= splits + splits / 10; ++s) {
             const long g = base * s;
             const double eff = (double)g / (double)(((g + slots - 1) / slots) * slots);
-            if (eff > best_eff + 1e-9) {
+            if (eff >= best_eff - 1e-9) {  // ties: the larger grid
                 best_eff = eff;
                 best = s;
             }
