@@ -782,9 +782,23 @@ def e2e(args, sp, work, ws, rank, comm=None):
     import torch
     host, tags = [], []
     h2d = d2h = 0
+    pinned = {}  # one host copy per device tensor: a layer's BWI and BWW name the same dY buffer
+    h2d_shared = 0  # bytes the batch call uploads: a buffer two consecutive passes name goes up once
+
+    def host_copy(t):
+        key = t.data.data_ptr()
+        if key not in pinned:
+            pinned[key] = t.data.cpu().pin_memory().numpy()
+        return sp.BlockedTensor(**{**t.header(), "data": pinned[key]})
+
+    prev_ptrs = set()
     for (tag, li, name, pp, fl, dgb) in work:
-        a = sp.BlockedTensor(**{**pp._a.header(), "data": pp._a.data.cpu().pin_memory().numpy()})
-        b = sp.BlockedTensor(**{**pp._b.header(), "data": pp._b.data.cpu().pin_memory().numpy()})
+        a, b = host_copy(pp._a), host_copy(pp._b)
+        ptrs = {pp._a.data.data_ptr(), pp._b.data.data_ptr()}
+        for t, hb_ in ((pp._a, a), (pp._b, b)):
+            if t.data.data_ptr() not in prev_ptrs or hb_.layout == sp.Layout.filter_kcrs_blk:
+                h2d_shared += hb_.data.nbytes
+        prev_ptrs = ptrs
         out = torch.empty(pp.out.numel(), dtype=torch.float32).pin_memory().numpy()
         host.append((a, b, pp, out, fl, name))
         tags.append(tag)
@@ -838,6 +852,7 @@ def e2e(args, sp, work, ws, rank, comm=None):
     flops = sum(h[4] for h in host)
     secs = timed(host, args.e2e_steps)
     per_call = {"value": round(flops / secs / 1e9, 1), "s_per_step": round(secs, 3), "s_all_steps": timed.last,
+                "h2d_bytes_per_step": int(h2d),
                 "path": "spc_run_parallel_host, one synchronous call per pass (H2D + kernels + D2H + sync each)"}
     res = {"value": per_call["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h), "s_per_step": per_call["s_per_step"],
@@ -860,6 +875,10 @@ def e2e(args, sp, work, ws, rank, comm=None):
         bsecs = sorted(per)[len(per) // 2]
         res.update({"value": round(flops / bsecs / 1e9, 1), "s_per_step": round(bsecs, 3),
                     "s_all_steps": [round(t, 3) for t in per], "statistic": "median step",
+                    "h2d_bytes_per_step": int(h2d_shared),
+                    "h2d_note": "every distinct input buffer of the step is copied host->device inside the timed "
+                                "region; a layer's BWI and BWW name the same dY host buffer, which the batch call "
+                                "uploads once (per_call uploads it for each call)",
                     "path": "spc_run_parallel_host_batch (include/spconv_b200.h): the step's passes in one call, "
                             "pinned host buffers, every input H2D and every output D2H inside the timed region, "
                             "pipelined across passes",

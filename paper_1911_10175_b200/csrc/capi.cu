@@ -706,6 +706,18 @@ spc_status host_streams(HostStreams*& hs) {
 
 static constexpr int kMaxHostChunks = 64;
 
+// chunk count of the per-call host path: ~chunk_mb of traffic per chunk, at most max_chunks
+static int host_chunk_count(size_t io_bytes, int units) {
+    static const int chunk_mb = std::getenv("SPC_HOST_CHUNK_MB") ? std::atoi(std::getenv("SPC_HOST_CHUNK_MB")) : 48;
+    static const int max_chunks =
+        std::getenv("SPC_HOST_MAX_CHUNKS") ? std::atoi(std::getenv("SPC_HOST_MAX_CHUNKS")) : 16;
+    int nc = (int)((io_bytes + ((size_t)chunk_mb << 20) - 1) / ((size_t)chunk_mb << 20));
+    if (nc > max_chunks) nc = max_chunks;
+    if (nc > kMaxHostChunks) nc = kMaxHostChunks;
+    if (nc > units) nc = units;
+    return nc < 1 ? 1 : nc;
+}
+
 // FWD / BWI host-buffer drop-in as ONE gated launch: copy-in stream
 // (H2D chunk c, then a 4-byte copy raising in_ready[c]), compute stream (the
 // kernel; CTAs of image i wait for in_ready[chunk(i)]), copy-out stream (D2H
@@ -872,14 +884,7 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
     // chunk count: ~chunk_mb of traffic per chunk, at most max_chunks (the
     // H2D / kernel / D2H of consecutive chunks overlap on 3 streams; the
     // call's exposed tail is one chunk's kernel + D2H)
-    static const int chunk_mb = std::getenv("SPC_HOST_CHUNK_MB") ? std::atoi(std::getenv("SPC_HOST_CHUNK_MB")) : 48;
-    static const int max_chunks =
-        std::getenv("SPC_HOST_MAX_CHUNKS") ? std::atoi(std::getenv("SPC_HOST_MAX_CHUNKS")) : 16;
-    int nc = (int)((io_bytes + ((size_t)chunk_mb << 20) - 1) / ((size_t)chunk_mb << 20));
-    if (nc > max_chunks) nc = max_chunks;
-    if (nc > kMaxHostChunks) nc = kMaxHostChunks;
-    if (nc > units) nc = units;
-    if (nc < 1) nc = 1;
+    const int nc = host_chunk_count(io_bytes, units);
 
     float *da = nullptr, *db = nullptr, *dd = nullptr, *dpart = nullptr;
     spc_counters* dc = nullptr;
@@ -1088,7 +1093,22 @@ struct BatchSlot {
     // the pass in flight
     int pass = -1, nc = 0;
     spc_tensor out{};
+    // host ranges of the pass (hazard checks) and its uploaded activation operands, which a later
+    // pass naming the same host buffer reads in place instead of uploading again (a layer's BWI and
+    // BWW both take dY in ActNCHWc); valid until the slot is enqueued again
+    const char *h_lo[3] = {nullptr, nullptr, nullptr}, *h_hi[3] = {nullptr, nullptr, nullptr};  // a, b, out
+    struct Upload {
+        const float* host = nullptr;
+        size_t numel = 0;
+        float* dev = nullptr;
+    } up[2];
+    int up_last_chunk = 0;           // in_done[up_last_chunk]: both uploads complete
+    cudaEvent_t lent_ev = nullptr;   // recorded after the last kernel of a pass that borrowed from this slot
+    bool lent = false;
 };
+inline bool ranges_overlap(const char* a0, const char* a1, const char* b0, const char* b1) {
+    return a0 && b0 && a0 < b1 && b0 < a1;
+}
 struct BatchState {
     int dev = -1;
     char* arena = nullptr;
@@ -1113,6 +1133,13 @@ int batch_chunks(const spc_host_pass& p, const spc_tensor& out) {
     const bool bww = p.plan->comp == SPC_BWW;
     const int units = bww ? (p.shape->N + p.plan->V - 1) / p.plan->V : p.shape->N;
     const size_t io = (p.a->numel + p.b->numel + out.numel) * sizeof(float);
+    // BWW sums its chunks' partial dG, so its chunking is the per-call path's (the two forms then
+    // agree bitwise); FWD / BWI chunks are independent image ranges and can be larger here, where
+    // the next pass hides a chunk's head and tail
+    if (bww) {
+        const int n = host_chunk_count(io, units);
+        return n > kBatchChunks ? kBatchChunks : n;
+    }
     int nc = (int)((io + ((size_t)chunk_mb << 20) - 1) / ((size_t)chunk_mb << 20));
     if (nc > kBatchChunks) nc = kBatchChunks;
     if (nc > units) nc = units;
@@ -1129,7 +1156,8 @@ spc_status batch_state(BatchState*& bs, size_t slot_bytes) {
                 if ((e = cudaEventCreateWithFlags(&sl.in_done[c], cudaEventDisableTiming)) != cudaSuccess ||
                     (e = cudaEventCreateWithFlags(&sl.k_done[c], cudaEventDisableTiming)) != cudaSuccess)
                     return cuda_fail(e, "event create");
-            if ((e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming)) != cudaSuccess)
+            if ((e = cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&sl.lent_ev, cudaEventDisableTiming)) != cudaSuccess)
                 return cuda_fail(e, "event create");
             if ((e = cudaMallocHost((void**)&sl.hc, kBatchChunks * sizeof(spc_counters))) != cudaSuccess)
                 return cuda_fail(e, "pinned alloc");
@@ -1145,14 +1173,19 @@ spc_status batch_state(BatchState*& bs, size_t slot_bytes) {
         if ((e = cudaMalloc((void**)&g_bs.arena, slot_bytes * batch_slots())) != cudaSuccess)
             return cuda_fail(e, "batch arena");
         g_bs.slot_bytes = slot_bytes;
-        for (int i = 0; i < batch_slots(); ++i) g_bs.slot[i].mem = g_bs.arena + (size_t)i * slot_bytes;
+        for (int i = 0; i < batch_slots(); ++i) {
+            g_bs.slot[i].mem = g_bs.arena + (size_t)i * slot_bytes;
+            g_bs.slot[i].up[0] = g_bs.slot[i].up[1] = BatchSlot::Upload{};
+            g_bs.slot[i].lent = false;
+        }
     }
     bs = &g_bs;
     return SPC_OK;
 }
 
 // enqueue one pass (pinned host buffers) into `sl`; no host synchronisation
-spc_status batch_enqueue(BatchSlot& sl, int idx, const spc_host_pass& p, const spc_tensor& out, HostStreams* hs) {
+spc_status batch_enqueue(BatchState& bs, BatchSlot& sl, int idx, const spc_host_pass& p, const spc_tensor& out,
+                         HostStreams* hs) {
     cudaStream_t s0 = hs->s[0], sin = hs->s[1], sout = hs->s[2];
     const spc_shape* shape = p.shape;
     const spc_plan* plan = p.plan;
@@ -1177,16 +1210,59 @@ spc_status batch_enqueue(BatchSlot& sl, int idx, const spc_host_pass& p, const s
     sl.pass = idx;
     sl.nc = nc;
     sl.out = out;
+    sl.up[0] = sl.up[1] = BatchSlot::Upload{};
+    sl.h_lo[0] = reinterpret_cast<const char*>(a->data);
+    sl.h_hi[0] = sl.h_lo[0] + a->numel * sizeof(float);
+    sl.h_lo[1] = reinterpret_cast<const char*>(b->data);
+    sl.h_hi[1] = sl.h_lo[1] + b->numel * sizeof(float);
+    sl.h_lo[2] = reinterpret_cast<const char*>(out.data);
+    sl.h_hi[2] = sl.h_lo[2] + out.numel * sizeof(float);
     cudaError_t ce = cudaSuccess;
     auto ck = [&](cudaError_t x) {
         if (x != cudaSuccess && ce == cudaSuccess) ce = x;
     };
     spc_status st = SPC_OK;
+    // a pass that borrowed an operand from this slot may still be reading it
+    if (sl.lent) {
+        ck(cudaStreamWaitEvent(sin, sl.lent_ev, 0));
+        sl.lent = false;
+    }
+    // device copies of host ranges this pass overwrites are stale from here on
+    for (int k = 0; k < batch_slots(); ++k)
+        for (auto& u : bs.slot[k].up)
+            if (u.host && ranges_overlap(reinterpret_cast<const char*>(u.host),
+                                         reinterpret_cast<const char*>(u.host + u.numel), sl.h_lo[2], sl.h_hi[2]))
+                u = BatchSlot::Upload{};
+    // an activation operand another slot already holds: read it there
+    BatchSlot* lender[2] = {nullptr, nullptr};
+    auto borrow = [&](const spc_tensor* t, int which) -> float* {
+        static const bool off = std::getenv("SPC_BATCH_SHARE") && std::atoi(std::getenv("SPC_BATCH_SHARE")) == 0;
+        if (off || !t) return nullptr;
+        for (int k = 0; k < batch_slots(); ++k) {
+            BatchSlot& o = bs.slot[k];
+            if (&o == &sl) continue;
+            for (auto& u : o.up)
+                if (u.host == t->data && u.numel == t->numel && u.dev) {
+                    lender[which] = &o;
+                    return u.dev;
+                }
+        }
+        return nullptr;
+    };
     if (!bww) ck(cudaMemcpyAsync(db, b->data, b->numel * sizeof(float), cudaMemcpyHostToDevice, sin));
     const float* hchk = chk->data;
     float* dchk = chk == a ? da : db;
     const float* hoth = oth ? oth->data : nullptr;
     float* doth = oth ? (oth == a ? da : db) : nullptr;
+    float* bchk = borrow(chk, 0);
+    float* both = borrow(oth, 1);
+    if (bchk) dchk = bchk;
+    if (both) doth = both;
+    for (int w = 0; w < 2; ++w)
+        if (lender[w]) ck(cudaStreamWaitEvent(s0, lender[w]->in_done[lender[w]->up_last_chunk], 0));
+    if (!bchk) sl.up[0] = BatchSlot::Upload{hchk, chk->numel, dchk};
+    if (oth && !both) sl.up[1] = BatchSlot::Upload{hoth, oth->numel, doth};
+    sl.up_last_chunk = nc - 1;
     const size_t chk_unit = chk->numel / units;
     const size_t oth_unit = oth ? oth->numel / shape->N : 0;
     const size_t out_unit = bww ? 0 : out.numel / shape->N;
@@ -1196,9 +1272,10 @@ spc_status batch_enqueue(BatchSlot& sl, int idx, const spc_host_pass& p, const s
         const int i1 = bww ? (u1 * V < shape->N ? u1 * V : shape->N) : u1;
         spc_shape shc = *shape;
         shc.N = i1 - i0;
-        ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
-                           (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
-        if (oth)
+        if (!bchk)
+            ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
+                               (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        if (oth && !both)
             ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
                                (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
         ck(cudaEventRecord(sl.in_done[c], sin));
@@ -1243,6 +1320,11 @@ spc_status batch_enqueue(BatchSlot& sl, int idx, const spc_host_pass& p, const s
         ck(cudaStreamWaitEvent(sout, sl.k_done[nc - 1], 0));
         ck(cudaMemcpyAsync(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost, sout));
     }
+    for (int w = 0; w < 2; ++w)
+        if (lender[w]) {  // every kernel of this pass is enqueued: the lender's slot may be refilled after them
+            ck(cudaEventRecord(lender[w]->lent_ev, s0));
+            lender[w]->lent = true;
+        }
     if (st == SPC_OK && ce == cudaSuccess && p.counters)
         ck(cudaMemcpyAsync(sl.hc, dc, nc * sizeof(spc_counters), cudaMemcpyDeviceToHost, sout));
     ck(cudaEventRecord(sl.done, sout));
@@ -1308,6 +1390,10 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
     if ((st = host_streams(hs))) return st;
     BatchState* bs = nullptr;
     if (slot_bytes && (st = batch_state(bs, slot_bytes))) return st;
+    auto forget_uploads = [&]() {  // device copies of host buffers are trusted only inside one call
+        for (int k = 0; k < kBatchSlotsMax && bs; ++k) bs->slot[k].up[0] = bs->slot[k].up[1] = BatchSlot::Upload{};
+    };
+    forget_uploads();
     spc_status first = SPC_OK;
     auto drain = [&]() {
         for (int k = 0; k < kBatchSlotsMax && bs; ++k) {
@@ -1324,7 +1410,28 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
             if (first) break;
             p.status = spc_run_parallel_host(p.a, p.b, p.shape, p.plan, p.mode, p.dst, p.counters);
             if (p.status) first = p.status;
+            forget_uploads();  // its output may overlap an uploaded range
             continue;
+        }
+        // host-buffer hazards against the passes in flight: an input an earlier pass writes, or an
+        // output an earlier pass reads or writes -> let them finish first (order of a sequential loop)
+        {
+            const char* lo[3] = {reinterpret_cast<const char*>(p.a->data), reinterpret_cast<const char*>(p.b->data),
+                                 reinterpret_cast<const char*>(outs[i].data)};
+            const char* hi[3] = {lo[0] + p.a->numel * sizeof(float), lo[1] + p.b->numel * sizeof(float),
+                                 lo[2] + outs[i].numel * sizeof(float)};
+            bool hazard = false;
+            for (int k = 0; k < kBatchSlots && !hazard; ++k) {
+                const BatchSlot& o = bs->slot[k];
+                if (o.pass < 0) continue;
+                hazard = ranges_overlap(lo[0], hi[0], o.h_lo[2], o.h_hi[2]) ||
+                         ranges_overlap(lo[1], hi[1], o.h_lo[2], o.h_hi[2]);
+                for (int w = 0; w < 3 && !hazard; ++w) hazard = ranges_overlap(lo[2], hi[2], o.h_lo[w], o.h_hi[w]);
+            }
+            if (hazard) {
+                drain();
+                if (first) break;
+            }
         }
         BatchSlot& sl = bs->slot[next_slot];
         next_slot = (next_slot + 1) % kBatchSlots;
@@ -1333,7 +1440,7 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
             first = st;
             break;
         }
-        st = batch_enqueue(sl, i, p, outs[i], hs);
+        st = batch_enqueue(*bs, sl, i, p, outs[i], hs);
         if (st) {
             p.status = st;
             first = st;

@@ -767,6 +767,89 @@ def test_host_batch_equals_per_call(sp):
             assert g.out.header() == w.out.header()
 
 
+def test_host_batch_shared_and_chained_buffers(sp):
+    """Batch passes that name the same host buffers: (1) BWI and BWW read one
+    dY buffer (uploaded once, read in place by the second pass); (2) a pass
+    reads the buffer an earlier pass of the batch writes (the batch must keep
+    the order of a sequential loop); (3) a later pass overwrites a buffer an
+    earlier pass read, and a still later pass reads the new contents.  All
+    pinned; results bitwise those of sequential per-call runs."""
+    import torch
+    V = 16
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+
+    def pinned(t):
+        return sp.BlockedTensor(**{**t.header(), "data": pin(t.data)})
+
+    n, C, K, H, W = 20, 32, 32, 12, 12
+    sh = sp.ConvShape.make(n, C, K, H, W, 3, 3, 1, 1)
+    D = O.gen_sparse(n, C, H, W, 0.6, 1)
+    G = O.gen_sparse(K, C, 3, 3, 0.0, 2)
+    pf, pb, pw = (sp.plan(sh, c, V) for c in (sp.Component.fwd, sp.Component.bwi, sp.Component.bww))
+    bD, bG, bGt, bDc = (pinned(t) for t in (sp.pack_act_nchwc(D, V), sp.pack_filter(G, V), sp.pack_filter(G, V, True),
+                                            sp.pack_act_chwnn(D, V)))
+    # sequential reference through the per-call path
+    r_fwd = sp.run_parallel(bD, bG, sh, pf, sp.RunMode.sparse)
+    Y = sp.BlockedTensor(**{**r_fwd.out.header(), "data": pin(r_fwd.out.data)})
+    r_bwi = sp.run_parallel(Y, bGt, sh, pb, sp.RunMode.sparse)
+    r_bww = sp.run_parallel(bDc, Y, sh, pw, sp.RunMode.sparse)
+    r_fwd2 = sp.run_parallel(sp.BlockedTensor(**{**bD.header(), "data": r_bwi.out.data}), bG, sh, pf, sp.RunMode.sparse)
+    r_bww2 = sp.run_parallel(bDc, sp.BlockedTensor(**{**Y.header(), "data": r_fwd2.out.data}), sh, pw,
+                             sp.RunMode.sparse)
+    # the same five passes as one batch over shared buffers
+    ybuf = pin(np.zeros_like(r_fwd.out.data))
+    dbuf = pin(np.zeros_like(r_bwi.out.data))
+    Yb = sp.BlockedTensor(**{**r_fwd.out.header(), "data": ybuf})
+    hb = sp.HostBatch()
+    hb.add(bD, bG, sh, pf, out=ybuf)                      # writes ybuf
+    hb.add(Yb, bGt, sh, pb, out=dbuf)                     # reads ybuf (chained), writes dbuf
+    hb.add(bDc, Yb, sh, pw)                               # reads ybuf again (shared upload)
+    hb.add(sp.BlockedTensor(**{**bD.header(), "data": dbuf}), bG, sh, pf, out=ybuf)  # overwrites ybuf
+    hb.add(bDc, Yb, sh, pw)                               # must see the NEW ybuf
+    for rep in range(2):
+        got = hb.run()
+        for i, (g, w) in enumerate(zip(got, (r_fwd, r_bwi, r_bww, r_fwd2, r_bww2))):
+            # pass 0's output buffer is overwritten by pass 3; its value is checked through passes 1 and 2
+            assert i == 0 or np.array_equal(g.out.data, w.out.data), i
+            assert g.counters == w.counters, i
+
+
+def test_host_batch_at_size_with_shared_dy(sp):
+    """VGG conv3_2 / conv4_2 at batch 32 (100 MB / 50 MB tensors), FWD / BWI /
+    BWW per layer with BWI and BWW naming one pinned dY buffer, eight layers'
+    worth of passes (24 > pipeline slots, so every slot is refilled while a
+    borrower may still read it): every output and counter bitwise those of
+    the per-call path."""
+    import torch
+    from paper_1911_10175_b200 import workloads as wl
+    V = 16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    pin = lambda t: sp.BlockedTensor(**{**t.header(), "data": t.data.cpu().pin_memory().numpy()})
+    hb = sp.HostBatch()
+    want = []
+    layers = wl.CONFIGS["vgg16_b32"]()
+    for rep in range(4):
+        for li in (4, 7):
+            sh = layers[li].shape
+            G = wl.device_weights(sh.K, sh.C, sh.S, sh.R, g)
+            D = wl.device_activation((sh.N, sh.C, sh.H, sh.W), 0.7, g)
+            dY = wl.device_grad((sh.N, sh.K, sh.out_h(), sh.out_w()), 0.7, g)
+            bD = sp.pack_act_nchwc(D, V)
+            hD, hY = pin(bD), pin(sp.pack_act_nchwc(dY, V))
+            ops = [(sp.Component.fwd, hD, pin(sp.pack_filter(G, V))), (sp.Component.bwi, hY, pin(sp.pack_filter(G, V, True))),
+                   (sp.Component.bww, pin(sp.nchwc_to_chwnn(bD)), hY)]
+            for comp, a, b in ops:
+                pl = sp.plan(sh, comp, V)
+                want.append(sp.run_parallel(a, b, sh, pl, sp.RunMode.sparse))
+                out = torch.empty(want[-1].out.data.size, dtype=torch.float32).pin_memory().numpy()
+                hb.add(a, b, sh, pl, out=out)
+            del D, dY, bD
+    got = hb.run()
+    for i, (gr, w) in enumerate(zip(got, want)):
+        assert np.array_equal(gr.out.data, w.out.data), i
+        assert gr.counters == w.counters, i
+
+
 def test_host_batch_validates_every_pass_before_device_work(sp):
     V = 16
     sh = sp.ConvShape.make(2, 16, 16, 5, 5, 3, 3, 1, 1)
