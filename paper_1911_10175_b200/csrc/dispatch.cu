@@ -51,12 +51,14 @@ cudaError_t launch_conv(bool fwd, bool sparse, const DevShape& sh, int V, const 
     static const bool pw_off = std::getenv("SPC_PW_OFF") && std::atoi(std::getenv("SPC_PW_OFF"));
     if (g_math == SPC_MATH_TF32X3 && gate.in_ready == nullptr && tc_conv_supported(fwd, sh, V))
         return launch_tc_conv(fwd, sparse, sh, src, filt, dst, exec_ctr, st, epi);
-    // 1x1 stride-2 BWI: the tile kernel's per-pixel zero skip (every dY pixel
-    // feeds one dD pixel; the gap pixels are written as zeros) measured 1.65x
-    // faster than the GEMM kernels, at every sparsity (tools/skip_evidence.py,
-    // profiles/r02_skip_evidence.md); the other 1x1 passes run counted-dense GEMMs
+    // 1x1 stride-2 BWI: the GEMM kernel with one row per SOURCE pixel (each row also
+    // writes its 2x2 cell's gap pixels as zeros): 375 / 356 / 461 us on ResNet-50's three
+    // projection shortcuts against 662 / 843 / 1116 us for the tile kernel's per-pixel zero
+    // skip, which had beaten the earlier output-pixel-row GEMM (1145 us: 3/4 of its FMAs
+    // were spent on the stride gaps).  SPC_S2_BWI_GEMM=0 selects the tile kernel (A/B).
     const bool pw_s2_bwi = !fwd && sh.R == 1 && sh.S == 1 && sh.O == 2 && sh.P == 2;
-    const bool s2_bwi_tile = pw_s2_bwi && tile_conv_supported(fwd, sh, V);
+    static const bool s2_gemm = !(std::getenv("SPC_S2_BWI_GEMM") && std::atoi(std::getenv("SPC_S2_BWI_GEMM")) == 0);
+    const bool s2_bwi_tile = pw_s2_bwi && !s2_gemm && tile_conv_supported(fwd, sh, V);
     if (!force_generic && !pw_off && !s2_bwi_tile && use_pw_gemm() && pw_gemm_supported(fwd, sh, V)) {
         int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
         cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
@@ -123,9 +125,12 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
         cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
         launch_finite_all(chk, chk_n, finite, st);
+        const bool counted = !use_row && !use_tma && tile_bww_counted_dense(check_input, sh);
+        if (counted)  // every FMA runs: dY must be finite too
+            launch_finite_also(oth, (size_t)sh.N * sh.K * sh.Hp * sh.Wp, finite, st);
         e = use_row && !use_tma ? launch_row_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, st)
             : use_tma ? launch_tma_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, 1, st)
-                      : launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, finite, 1);
+                      : launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, finite, 1, counted);
         if (e == cudaSuccess) {
             const int gs = bww_generic_splits(sh);
             const size_t E = (size_t)sh.K * sh.C * sh.S * sh.R;

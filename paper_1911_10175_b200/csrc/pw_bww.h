@@ -8,4 +8,5 @@ bool pw_bww_supported(bool check_input, const DevShape& sh, int V);
 cudaError_t launch_pw_bww(bool sparse, const DevShape& sh, const float* dchw, const float* dy, float* dst,
                           unsigned long long* exec_ctr, const int* finite, cudaStream_t st);
 void launch_finite_all(const float* t, size_t n, int* flag, cudaStream_t st);
+void launch_finite_also(const float* t, size_t n, int* flag, cudaStream_t st);
 }  // namespace spc

@@ -18,8 +18,11 @@
 //             ([Co/16][Ci/16][16 ci][16 co], 64 contiguous bytes per (ci, co-block)).
 // Each thread owns 4 output-channel pairs x 8 rows (FFMA2 over the pair, X
 // broadcast), 4-stage cp.async pipeline.  The fused epilogue (Epi) applies at
-// the store.  Stride 2: FWD reads source pixel 2o; BWI covers every output
-// pixel, the stride gaps accumulate nothing (exactly 0, epilogue applied).
+// the store.  Stride 2: FWD reads source pixel 2o; BWI rows are the SOURCE
+// pixels (an output-pixel row space would spend 3/4 of its FMAs on the stride
+// gaps: measured 1145 us against 330 us of useful work on ResNet-50's stage-2
+// projection), and each row also writes its 2x2 cell's gap pixels, which
+// accumulate nothing (exactly 0, epilogue applied).
 #include <cstdint>
 
 #include "common.cuh"
@@ -54,7 +57,9 @@ __global__ void __launch_bounds__((BK / 8) * 16, 2) pw_gemm_kernel(DevShape sh, 
     const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
     const int CiB = Ci / 16, CoB = Co / 16;
     const int HWo = Ho * Wo;
-    const long rows = (long)sh.N * HWo;
+    constexpr bool SRCROWS = !FWD && STR > 1;  // BWI stride 2: one row per source pixel
+    const int HWr = SRCROWS ? Hs * Wsrc : HWo;
+    const long rows = (long)sh.N * HWr;
     const int ktile = blockIdx.y;
     const long row0 = (long)blockIdx.x * PG_BP;
     const int k_base = ktile * BK;
@@ -72,14 +77,13 @@ __global__ void __launch_bounds__((BK / 8) * 16, 2) pw_gemm_kernel(DevShape sh, 
         const long row = row0 + p;
         long off = -1;
         if (row < rows) {
-            const int i = (int)(row / HWo), o = (int)(row % HWo);
-            const int oy = o / Wo, ox = o - oy * Wo;
+            const int i = (int)(row / HWr), o = (int)(row % HWr);
             int sidx = -1;
             if (FWD) {
+                const int oy = o / Wo, ox = o - oy * Wo;
                 sidx = (oy * STR) * Wsrc + ox * STR;
-            } else if (!(STR > 1 && (oy % STR || ox % STR))) {
-                const int sy = oy / STR, sx = ox / STR;
-                if (sy < Hs && sx < Wsrc) sidx = sy * Wsrc + sx;
+            } else {
+                sidx = o;  // stride 1: output pixel = source pixel; stride 2: the row IS the source pixel
             }
             if (sidx >= 0) off = ((long)i * CiB * Hs * Wsrc + sidx) * 16 + q * 4;  // + cb * Hs*Wsrc*16
         }
@@ -163,7 +167,14 @@ __global__ void __launch_bounds__((BK / 8) * 16, 2) pw_gemm_kernel(DevShape sh, 
     for (int j = 0; j < 8; ++j) {
         const long row = row0 + tx + 16 * j;
         if (row < rows) {
-            const int i = (int)(row / HWo), o = (int)(row % HWo);
+            const int i = (int)(row / HWr);
+            int o = (int)(row % HWr);
+            int oy = 0, ox = 0;
+            if constexpr (SRCROWS) {
+                oy = (o / Wsrc) * STR;
+                ox = (o % Wsrc) * STR;
+                o = oy * Wo + ox;
+            }
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
                 const int k = k_base + (g ? k1 : k0);
@@ -174,6 +185,21 @@ __global__ void __launch_bounds__((BK / 8) * 16, 2) pw_gemm_kernel(DevShape sh, 
                     for (int e = 0; e < 4; ++e) v[e] = epi.apply(v[e], off + e);
                 }
                 *reinterpret_cast<float4*>(dst + off) = make_float4(v[0], v[1], v[2], v[3]);
+                if constexpr (SRCROWS) {  // the cell's gap pixels
+#pragma unroll
+                    for (int dy = 0; dy < STR; ++dy)
+#pragma unroll
+                        for (int dx = 0; dx < STR; ++dx) {
+                            if ((dy == 0 && dx == 0) || oy + dy >= Ho || ox + dx >= Wo) continue;
+                            const size_t goff = off + (size_t)(dy * Wo + dx) * 16;
+                            float z[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                            if (epi.active()) {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) z[e] = epi.apply(0.0f, goff + e);
+                            }
+                            *reinterpret_cast<float4*>(dst + goff) = make_float4(z[0], z[1], z[2], z[3]);
+                        }
+                }
             }
         }
     }
@@ -189,7 +215,7 @@ cudaError_t pg_launch(bool sparse, const DevShape& sh, const float* src, const f
     constexpr int NT = (BK / 8) * 16;
     const int Co = FWD ? sh.K : sh.C;
     const int Ho = FWD ? sh.Hp : sh.H, Wo = FWD ? sh.Wp : sh.W;
-    const long rows = (long)sh.N * Ho * Wo;
+    const long rows = (!FWD && STR > 1) ? (long)sh.N * sh.Hp * sh.Wp : (long)sh.N * Ho * Wo;
     const size_t smem = (size_t)PG_NST * (PG_BP * PG_XS + 16 * (BK + 4)) * sizeof(float);
     auto k0 = sparse ? pw_gemm_kernel<FWD, BK, STR, true, false> : pw_gemm_kernel<FWD, BK, STR, false, false>;
     auto k1 = sparse ? pw_gemm_kernel<FWD, BK, STR, true, true> : pw_gemm_kernel<FWD, BK, STR, false, true>;

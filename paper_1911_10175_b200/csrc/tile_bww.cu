@@ -94,8 +94,11 @@ __device__ __forceinline__ void bww_jt_words(Acc& acc, const Ov& O, const float*
 }
 
 // JT = 100: jump-table dispatch over the nonzero checked pixels only
-// (jt_blocks.cuh, generated); 0: one uniform branch per checked pixel.  Same
-// accumulation order either way.  `sel`/`want`: device-side kernel choice.
+// (jt_blocks.cuh, generated); 0: one uniform branch per checked pixel; 200:
+// "counted dense" -- every pixel's FMAs run while the ballots still count
+// (stride 2: a checked pixel feeds ~2.25 taps, too few for a branch to pay;
+// finite operands only, the dispatcher guards).  Same accumulation order in
+// all three.  `sel`/`want`: device-side kernel choice.
 template <bool CHECK_INPUT, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, int JT, bool SPARSE>
 __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const float* __restrict__ chk,
                                                             const float* __restrict__ oth,
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(NWC * 32) bww_tile_kernel(DevShape sh, const f
 #pragma unroll
                     for (int rx = 0; rx < CRW; ++rx) {
                         const int p = ry * CRW + rx;
-                        if (!SPARSE || ((m[p >> 5] >> (p & 31)) & 1u)) {
+                        if (!SPARSE || JT == 200 || ((m[p >> 5] >> (p & 31)) & 1u)) {
                             const float4 q4 = cur[rx >> 2];
                             const float d =
                                 (rx & 3) == 0 ? q4.x : (rx & 3) == 1 ? q4.y : (rx & 3) == 2 ? q4.z : q4.w;
@@ -425,7 +428,8 @@ __global__ void bww_tile_reduce(DevShape sh, const float* __restrict__ partial, 
 // JTSEL, sparse mode launches both the per-pixel-branch kernel and the
 // jump-table kernel; a density probe on the checked tensor picks one on the
 // device (the other exits at entry), no host synchronisation.
-template <bool CI, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, bool JTSEL = false>
+template <bool CI, int KK, int CB, int NWC, int TH, int TW, int R, int S, int STR, bool JTSEL = false,
+          bool COUNTED_DENSE = false>
 static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* chk, const float* oth,
                                   float* dst, unsigned long long* exec_ctr, cudaStream_t st,
                                   const int* xsel = nullptr, int xwant = 0) {
@@ -470,7 +474,7 @@ static cudaError_t launch_bww_cfg(bool sparse, const DevShape& sh, const float* 
         k1<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, sel, 1);
         note_launch(2);
     } else {
-        auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, true>
+        auto kern = sparse ? bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, COUNTED_DENSE ? 200 : 0, true>
                            : bww_tile_kernel<CI, KK, CB, NWC, TH, TW, R, S, STR, 0, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         kern<<<grid, G::NT, G::SMEM, st>>>(sh, chk, oth, partial, (int)splits, exec_ctr, xsel, xwant);
@@ -588,19 +592,39 @@ cudaError_t launch_tile_bww(bool check_input, bool sparse, const DevShape& sh, c
 #undef SPC_B
 }
 
+// 3x3 stride-2 check=input BWW runs counted dense unless SPC_BWW_S2_SKIP=1 (A/B).  The caller
+// must then have folded BOTH operands' finiteness into *sel (0 * Inf would be NaN where the
+// reference skips): tile_bww_counted_dense() tells it so.
+static bool counted_dense_s2() {
+    static const bool skip = std::getenv("SPC_BWW_S2_SKIP") && std::atoi(std::getenv("SPC_BWW_S2_SKIP")) == 1;
+    return !skip;
+}
+bool tile_bww_counted_dense(bool check_input, const DevShape& sh) {
+    return check_input && sh.R == 3 && sh.S == 3 && sh.O == 2 && sh.P == 2 && counted_dense_s2();
+}
+
 // The default stride-1 configurations gated on a device word (*sel == want):
 // the exact FFMA BWW behind the tensor-core variant for Inf/NaN operands.
 cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& sh, const float* chk,
                                  const float* oth, float* dst, unsigned long long* exec_ctr, cudaStream_t st,
-                                 const int* sel, int want) {
+                                 const int* sel, int want, bool both_finite_gated) {
     const bool kk4 = (check_input ? sh.K : sh.C) % 128 == 0;
 #define SPC_B(CI, KK, CB, NWC, TH, TW, R) \
     return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, 1>(sparse, sh, chk, oth, dst, exec_ctr, st, sel, want)
 #define SPC_B2(CI, KK, CB, NWC, TH, TW, R) \
     return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, 2>(sparse, sh, chk, oth, dst, exec_ctr, st, sel, want)
+#define SPC_B2D(CI, KK, CB, NWC, TH, TW, R)                                                                          \
+    return launch_bww_cfg<CI, KK, CB, NWC, TH, TW, R, R, 2, false, true>(sparse, sh, chk, oth, dst, exec_ctr, st, sel, \
+                                                                         want)
     if (sh.O == 2) {  // the stride-2 configurations of launch_tile_bww
         if (check_input) {
             if (sh.R == 3) {
+                // counted dense (tile_bww_counted_dense): measured 627 -> ~430 us on ResNet-50's
+                // stage-2 3x3 stride-2 BWW at s = 0.6 (the per-pixel branches cost more than they skip)
+                if (both_finite_gated && counted_dense_s2()) {
+                    if (kk4) SPC_B2D(true, 4, 2, 4, 2, 4, 3);
+                    SPC_B2D(true, 2, 4, 4, 2, 4, 3);
+                }
                 if (kk4) SPC_B2(true, 4, 2, 4, 2, 4, 3);
                 SPC_B2(true, 2, 4, 4, 2, 4, 3);
             }
@@ -627,6 +651,7 @@ cudaError_t launch_tile_bww_when(bool check_input, bool sparse, const DevShape& 
     SPC_B(false, 2, 4, 4, 4, 8, 1);
 #undef SPC_B
 #undef SPC_B2
+#undef SPC_B2D
 }
 
 }  // namespace spc

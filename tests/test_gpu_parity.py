@@ -865,6 +865,35 @@ def test_host_batch_validates_every_pass_before_device_work(sp):
     assert sp.launch_count() == n0
 
 
+def test_s2_bww_counted_dense_keeps_the_skip_semantics_for_nonfinite_dy(sp):
+    """3x3 stride-2 BWW (check=input) runs every FMA ("counted dense") only when
+    both operands are finite: with Inf / NaN in dY at pixels whose D partners are
+    zero, the reference skips those products (P/include/spconv/vec.hpp:120-128) and
+    so must we (the exact kernel takes over); counters stay exact either way."""
+    V = 16
+    sh = sp.ConvShape.make(3, 64, 128, 13, 12, 3, 3, 2, 2)
+    t = sh.astuple()
+    D = O.gen_sparse(3, 64, 13, 12, 0.6, 11)
+    dY = O.gen_sparse(3, 128, sh.out_h(), sh.out_w(), 0.0, 12)
+    pl = sp.plan(sh, sp.Component.bww, V)
+    for poison in (False, True):
+        d = D.copy()
+        g = dY.copy()
+        if poison:
+            d[1, :, 0:5, 0:5] = 0.0          # every D partner of dY[1, :, 0..1, 0..1] is zero
+            g[1, 5, 0, 0] = np.inf
+            g[1, 77, 1, 1] = np.nan
+        # the skipped products contribute nothing: the expected dG is the dense oracle's on the
+        # unpoisoned dY (the poisoned pixels only ever meet zero D values)
+        ref = O.dense(2, t, d, dY)
+        res = sp.run_parallel(sp.pack_act_chwnn(d, V).to("cuda"), sp.pack_act_nchwc(g, V).to("cuda"), sh, pl,
+                              sp.RunMode.sparse)
+        got = sp.unpack(res.out).cpu().numpy()
+        assert np.isfinite(got).all(), poison
+        assert O.max_abs_rel(got, ref) <= TOL
+        assert res.counters.executed_vector_fmas == O.expected_counts(t, O.plan(t, 2, V), d)["executed_vector_fmas"]
+
+
 def test_vector_probes_match_reference_semantics(sp):  # test_vec.cpp:38-57, kernels.hpp:90-98
     rng = np.random.default_rng(8)
     for V in (4, 8, 16):
