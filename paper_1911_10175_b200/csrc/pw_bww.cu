@@ -171,7 +171,9 @@ __global__ void __launch_bounds__((BK / 8) * (BC / 8)) pw_bww_kernel(DevShape sh
 }
 
 // fixed-order split sum -> FilterKCRSblk (K, C), R = S = 1
-__global__ void pw_bww_reduce(int C, int K, const float* __restrict__ partial, int splits, float* __restrict__ dst) {
+__global__ void pw_bww_reduce(int C, int K, const float* __restrict__ partial, int splits, float* __restrict__ dst,
+                              const int* __restrict__ only_if_nonfinite) {
+    if (only_if_nonfinite != nullptr && __ldg(only_if_nonfinite) != 0) return;
     const size_t E = (size_t)C * K;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < E; e += (size_t)gridDim.x * blockDim.x) {
         float s = 0.0f;
@@ -197,7 +199,7 @@ __global__ void set_one_kernel(int* flag) { *flag = 1; }
 
 template <int BK, int BC, int STR>
 cudaError_t pb_launch(bool sparse, const DevShape& sh, const float* dchw, const float* dy, float* dst,
-                      unsigned long long* exec_ctr, const int* finite, cudaStream_t st) {
+                      unsigned long long* exec_ctr, const int* finite, cudaStream_t st, bool exact_only) {
     constexpr int NT = (BK / 8) * (BC / 8);
     const size_t smem = (size_t)PB_NST * (BC * PB_DS + (BK / 2) * PB_YS) * sizeof(float);
     const long tiles = (long)(sh.K / BK) * (sh.C / BC);
@@ -213,14 +215,15 @@ cudaError_t pb_launch(bool sparse, const DevShape& sh, const float* dchw, const 
     cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(sh.K / BK, sh.C / BC, (unsigned)splits);
-    k0<<<grid, NT, smem, st>>>(sh, dchw, dy, partial, (int)splits, exec_ctr, finite);
+    // exact_only: the finite case is tma_pw_bww.cu's (already enqueued); this is its Inf / NaN fallback
+    if (!exact_only) k0<<<grid, NT, smem, st>>>(sh, dchw, dy, partial, (int)splits, exec_ctr, finite);
     k1<<<grid, NT, smem, st>>>(sh, dchw, dy, partial, (int)splits, exec_ctr, finite);
-    note_launch(2);
+    note_launch(exact_only ? 1 : 2);
     e = cudaGetLastError();
     if (e == cudaSuccess) {
         unsigned rb = (unsigned)(((size_t)sh.C * sh.K + 255) / 256);
         if (rb > 148 * 8) rb = 148 * 8;
-        pw_bww_reduce<<<rb, 256, 0, st>>>(sh.C, sh.K, partial, (int)splits, dst);
+        pw_bww_reduce<<<rb, 256, 0, st>>>(sh.C, sh.K, partial, (int)splits, dst, exact_only ? finite : nullptr);
         note_launch();
         e = cudaGetLastError();
     }
@@ -239,9 +242,16 @@ bool pw_bww_supported(bool check_input, const DevShape& sh, int V) {
 cudaError_t launch_pw_bww(bool sparse, const DevShape& sh, const float* dchw, const float* dy, float* dst,
                           unsigned long long* exec_ctr, const int* finite, cudaStream_t st) {
     const bool k128 = sh.K % 128 == 0, c128 = sh.C % 128 == 0;
-#define PB_L(BK, BC)                                                                                   \
-    return sh.O == 1 ? pb_launch<BK, BC, 1>(sparse, sh, dchw, dy, dst, exec_ctr, finite, st)          \
-                     : pb_launch<BK, BC, 2>(sparse, sh, dchw, dy, dst, exec_ctr, finite, st)
+    // finite dY: the TMA-staged GEMM (tma_pw_bww.cu); this file's EXACT kernel stays its Inf / NaN fallback
+    bool exact_only = false;
+    if (tma_pw_bww_supported(sh)) {
+        const cudaError_t e = launch_tma_pw_bww(sparse, sh, dchw, dy, dst, exec_ctr, finite, st);
+        if (e != cudaSuccess) return e;
+        exact_only = true;
+    }
+#define PB_L(BK, BC)                                                                                       \
+    return sh.O == 1 ? pb_launch<BK, BC, 1>(sparse, sh, dchw, dy, dst, exec_ctr, finite, st, exact_only)  \
+                     : pb_launch<BK, BC, 2>(sparse, sh, dchw, dy, dst, exec_ctr, finite, st, exact_only)
     if (k128 && c128) PB_L(128, 128);
     if (k128) PB_L(128, 64);
     if (c128) PB_L(64, 128);

@@ -327,6 +327,10 @@ __global__ void __launch_bounds__(NWC * 32, MINB)
                 }
             }
         }
+        // generic-proxy reads of this stage (the LDS above) must be ordered before the async-proxy
+        // TMA write that refills it: the empty barrier's release does not cross proxies
+        // (tma_pw_bww.cu measured the race on short steps; same protocol here)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_bar(s));
     }
