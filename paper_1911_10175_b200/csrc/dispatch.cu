@@ -124,12 +124,12 @@ cudaError_t launch_bww(bool check_input, bool sparse, const DevShape& sh, int V,
         int* finite = stream_flags(st) ? stream_flags(st) + FLAG_FINITE : nullptr;
         cudaError_t e = finite ? cudaSuccess : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) return e;
-        launch_finite_all(chk, chk_n, finite, st);
+        if (!use_tma) launch_finite_all(chk, chk_n, finite, st);  // the TMA kernel's pre-pass scans as it transposes
         const bool counted = !use_row && !use_tma && tile_bww_counted_dense(check_input, sh);
         if (counted)  // every FMA runs: dY must be finite too
             launch_finite_also(oth, (size_t)sh.N * sh.K * sh.Hp * sh.Wp, finite, st);
         e = use_row && !use_tma ? launch_row_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, st)
-            : use_tma ? launch_tma_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, 1, st)
+            : use_tma ? launch_tma_bww_when(sparse, sh, chk, oth, dst, exec_ctr, finite, 1, st, finite)
                       : launch_tile_bww_when(check_input, sparse, sh, chk, oth, dst, exec_ctr, st, finite, 1, counted);
         if (e == cudaSuccess) {
             const int gs = bww_generic_splits(sh);

@@ -259,6 +259,11 @@ cudaError_t launch_pw_bww(bool sparse, const DevShape& sh, const float* dchw, co
 #undef PB_L
 }
 
+void launch_set_flag(int* flag, cudaStream_t st) {
+    set_one_kernel<<<1, 1, 0, st>>>(flag);
+    note_launch();
+}
+
 // AND another tensor's finiteness into a flag launch_finite_all already wrote
 void launch_finite_also(const float* t, size_t n, int* flag, cudaStream_t st) {
     finite_all_kernel<<<148 * 4, 256, 0, st>>>(t, n, flag);

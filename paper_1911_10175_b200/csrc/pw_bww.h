@@ -12,5 +12,6 @@ bool tma_pw_bww_supported(const DevShape& sh);
 cudaError_t launch_tma_pw_bww(bool sparse, const DevShape& sh, const float* dchw, const float* dy, float* dst,
                               unsigned long long* exec_ctr, const int* finite, cudaStream_t st);
 void launch_finite_all(const float* t, size_t n, int* flag, cudaStream_t st);
+void launch_set_flag(int* flag, cudaStream_t st);  // *flag = 1
 void launch_finite_also(const float* t, size_t n, int* flag, cudaStream_t st);
 }  // namespace spc

@@ -27,8 +27,11 @@ cudaError_t launch_row_bww_when(bool sparse, const DevShape& sh, const float* ch
 
 // tma_bww.cu: check = input, 3x3 stride 1 pad 1, K % 128 == 0 (TMA-staged tile kernel)
 bool tma_bww_supported(bool check_input, const DevShape& sh, int V);
-// runs when *sel == want (sel == nullptr: always)
+// runs when *sel == want (sel == nullptr: always).  scan_flag (normally == sel, want == 1): the kernel's
+// pre-pass over the checked tensor also is its finiteness scan -- it presets the flag to 1 and clears it
+// on Inf / NaN, replacing a separate launch_finite_all
 cudaError_t launch_tma_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
-                                unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st);
+                                unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st,
+                                int* scan_flag = nullptr);
 
 }  // namespace spc

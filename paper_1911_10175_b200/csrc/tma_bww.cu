@@ -22,6 +22,7 @@
 // split reduction are those of tile_bww.cu.
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "pw_bww.h"
 #include "tile_bww.h"
 
 #include <cstdlib>
@@ -68,9 +69,13 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 // the tensor map's x extent is W + 1.
 __global__ void __launch_bounds__(256) chwnn_to_planes_kernel(const float* __restrict__ src, float* __restrict__ dst,
                                                               int N, int C, int H, int W, int Wpitch,
-                                                              const int* __restrict__ sel, int want) {
-    if (sel != nullptr && __ldg(sel) != want) return;
+                                                              const int* __restrict__ sel, int want,
+                                                              int* __restrict__ finite_out) {
+    // finite_out: this pass is also the finiteness scan of the checked tensor (flag preset to 1,
+    // cleared on Inf / NaN) -- it reads every element anyway; it then runs ungated
+    if (finite_out == nullptr && sel != nullptr && __ldg(sel) != want) return;
     __shared__ float s[256][17];
+    int bad = 0;
     const int HW = H * W;
     const int nb = blockIdx.z, c = blockIdx.y, p0 = blockIdx.x * 256;
     const int npx = HW - p0 < 256 ? HW - p0 : 256;
@@ -79,7 +84,9 @@ __global__ void __launch_bounds__(256) chwnn_to_planes_kernel(const float* __res
         const float4 v = __ldg(in + e);
         float* r = &s[e >> 2][(e & 3) * 4];
         r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+        bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
     }
+    if (finite_out != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(finite_out, 0);
     __syncthreads();
     const int nimg = N - nb * 16 < 16 ? N - nb * 16 : 16;
     if ((int)threadIdx.x < npx) {
@@ -371,7 +378,7 @@ __global__ void tma_bww_reduce(DevShape sh, const float* __restrict__ partial, i
 
 template <int KK, int CB, int NWC, int TH, int TW, int MINB, int NSTAGE = 4>
 cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
-                       unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st) {
+                       unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st, int* scan_flag) {
     using G = TGeom<KK, CB, NWC, TH, TW, NSTAGE>;
     if (!tc::encode_fn()) return cudaErrorNotSupported;
     const int Wpitch = (sh.W + 1 + 3) / 4 * 4;
@@ -420,9 +427,10 @@ cudaError_t launch_cfg(bool sparse, const DevShape& sh, const float* chk, const 
         return e;
     }
     const int HW = sh.H * sh.W;
+    if (scan_flag != nullptr) launch_set_flag(scan_flag, st);
     chwnn_to_planes_kernel<<<dim3((HW + 255) / 256, sh.C, (sh.N + 15) / 16), 256, 0, st>>>(chk, planes, sh.N, sh.C,
                                                                                              sh.H, sh.W, Wpitch, sel,
-                                                                                             want);
+                                                                                             want, scan_flag);
     note_launch();
 
     CUtensorMap mapD, mapY;
@@ -498,30 +506,31 @@ bool tma_bww_supported(bool check_input, const DevShape& sh, int V) {
 }
 
 cudaError_t launch_tma_bww_when(bool sparse, const DevShape& sh, const float* chk, const float* oth, float* dst,
-                                unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st) {
+                                unsigned long long* exec_ctr, const int* sel, int want, cudaStream_t st,
+                                int* scan_flag) {
 #ifdef SPC_DEV
     if (sh.K % 128 != 0) {  // 64-channel lane blocks: KK = 2
         switch (tma_cfg()) {
-        case 11: return launch_cfg<2, 2, 8, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-        case 12: return launch_cfg<2, 2, 4, 7, 4, 4>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-        case 13: return launch_cfg<2, 4, 4, 7, 4, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-        default: return launch_cfg<2, 1, 8, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
+        case 11: return launch_cfg<2, 2, 8, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+        case 12: return launch_cfg<2, 2, 4, 7, 4, 4>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+        case 13: return launch_cfg<2, 4, 4, 7, 4, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+        default: return launch_cfg<2, 1, 8, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
         }
     }
     switch (tma_cfg()) {
-    case 1: return launch_cfg<4, 2, 4, 7, 2, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 2: return launch_cfg<4, 2, 4, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 3: return launch_cfg<4, 1, 8, 7, 2, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 4: return launch_cfg<4, 2, 8, 7, 2, 1>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 5: return launch_cfg<4, 1, 4, 7, 4, 4>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 7: return launch_cfg<4, 1, 8, 7, 2, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 8: return launch_cfg<4, 1, 8, 7, 4, 2, 6>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
-    case 9: return launch_cfg<4, 1, 8, 7, 4, 2, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
+    case 1: return launch_cfg<4, 2, 4, 7, 2, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 2: return launch_cfg<4, 2, 4, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 3: return launch_cfg<4, 1, 8, 7, 2, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 4: return launch_cfg<4, 2, 8, 7, 2, 1>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 5: return launch_cfg<4, 1, 4, 7, 4, 4>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 7: return launch_cfg<4, 1, 8, 7, 2, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 8: return launch_cfg<4, 1, 8, 7, 4, 2, 6>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
+    case 9: return launch_cfg<4, 1, 8, 7, 4, 2, 3>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
     default: break;
     }
 #endif
     // KK = 4 lane channels per lane, one checked channel per warp, 8 warps, 7x4 tile, 2 CTAs / SM
-    return launch_cfg<4, 1, 8, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st);
+    return launch_cfg<4, 1, 8, 7, 4, 2>(sparse, sh, chk, oth, dst, exec_ctr, sel, want, st, scan_flag);
 }
 
 }  // namespace spc
