@@ -894,6 +894,28 @@ def test_s2_bww_counted_dense_keeps_the_skip_semantics_for_nonfinite_dy(sp):
         assert res.counters.executed_vector_fmas == O.expected_counts(t, O.plan(t, 2, V), d)["executed_vector_fmas"]
 
 
+def test_tma_pw_bww_stage_reuse_is_race_free(sp):
+    """The TMA-staged 1x1 BWW GEMM on a shape whose CTAs reuse their pipeline
+    stages (56x56 images, K = 64: short steps).  Before the proxy fence that
+    orders the warps' reads of a stage against its TMA refill, this shape gave
+    ~1e-4 relative errors that changed from run to run (csrc/tma_pw_bww.cu)."""
+    V = 16
+    n, C, K, H, W = 16, 256, 64, 56, 56
+    sh = sp.ConvShape.make(n, C, K, H, W, 1, 1, 1, 1)
+    D = O.gen_sparse(n, C, H, W, 0.5, 1)
+    dY = O.gen_sparse(n, K, H, W, 0.0, 2)
+    ref = O.dense(2, sh.astuple(), D, dY)
+    pl = sp.plan(sh, sp.Component.bww, V)
+    a, b = sp.pack_act_chwnn(D, V).to("cuda"), sp.pack_act_nchwc(dY, V).to("cuda")
+    first = None
+    for rep in range(4):
+        got = sp.unpack(sp.run_parallel(a, b, sh, pl, sp.RunMode.sparse).out).cpu().numpy()
+        assert O.max_abs_rel(got, ref) <= TOL, rep
+        if first is None:
+            first = got
+        assert np.array_equal(got, first), rep
+
+
 def test_vector_probes_match_reference_semantics(sp):  # test_vec.cpp:38-57, kernels.hpp:90-98
     rng = np.random.default_rng(8)
     for V in (4, 8, 16):
