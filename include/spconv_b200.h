@@ -4,11 +4,12 @@
  * Drop-in replacement for the hot path of the reference `spconv` library
  * (SparseTrain, arXiv 1911.10175): the three training passes FWD / BWI / BWW
  * over dense blocked fp32 tensors that skip work on zeros ReLU puts into the
- * checked tensor.  Zero skipping is per element on 3x3 stride-1 passes, 3x3
- * stride-2 BWI/BWW and 1x1 stride-2 BWI; 1x1 FWD/BWW, 1x1 stride-1 BWI and
- * 3x3 stride-2 FWD execute every FMA ("counted dense": measured faster than
- * any skip granularity on B200, profiles/r02_skip_evidence.md) with the
- * reference's exact counters and Inf/NaN semantics.
+ * checked tensor.  Zero skipping is per element on the 3x3 stride-1 passes
+ * (FWD / BWI / BWW), 3x3 stride-2 BWI and BWW with check = output_grad; the
+ * 1x1 passes and 3x3 stride-2 FWD / BWW (check = input) execute every FMA
+ * ("counted dense": measured faster than any skip granularity on B200,
+ * profiles/r02_skip_evidence.md) with the reference's exact
+ * counters and Inf/NaN semantics.
  * Every entry point below replaces one reference interface
  * (cited as P/<file>:<line>, P = /root/reference/proj):
  *
@@ -24,6 +25,8 @@
  *   spc_relu / spc_relu_grad_mask <- relu / relu_grad_mask  P/include/spconv/sparsity.hpp:14-18
  *   spc_gen_sparse      <- spconv::gen_sparse    P/include/spconv/sparsity.hpp (P/src/sparsity.cpp:42-55)
  *   spc_vector_probes   <- spconv::vector_probes P/include/spconv/kernels.hpp:90-98
+ *   spc_run_parallel_host_batch <- the harness loop over layers and components,
+ *                       one run_parallel per pass (P/src/bench.cpp:216-288), as one call
  *   spc_bww_allreduce / spc_bww_sharded / spc_comm_*: no reference counterpart
  *                       (the reference is single-process, P/src/kernels.cpp:76-102);
  *                       the batch-sharded BWW exchange of SURVEY.md 8(e)
