@@ -783,7 +783,6 @@ def e2e(args, sp, work, ws, rank, comm=None):
     host, tags = [], []
     h2d = d2h = 0
     pinned = {}  # one host copy per device tensor: a layer's BWI and BWW name the same dY buffer
-    h2d_shared = 0  # bytes the batch call uploads: a buffer two consecutive passes name goes up once
 
     def host_copy(t):
         key = t.data.data_ptr()
@@ -791,14 +790,11 @@ def e2e(args, sp, work, ws, rank, comm=None):
             pinned[key] = t.data.cpu().pin_memory().numpy()
         return sp.BlockedTensor(**{**t.header(), "data": pinned[key]})
 
-    prev_ptrs = set()
+    fwd_a = {}  # (sparsity tag, layer) -> the FWD pass's ActNCHWc input D on the host
     for (tag, li, name, pp, fl, dgb) in work:
         a, b = host_copy(pp._a), host_copy(pp._b)
-        ptrs = {pp._a.data.data_ptr(), pp._b.data.data_ptr()}
-        for t, hb_ in ((pp._a, a), (pp._b, b)):
-            if t.data.data_ptr() not in prev_ptrs or hb_.layout == sp.Layout.filter_kcrs_blk:
-                h2d_shared += hb_.data.nbytes
-        prev_ptrs = ptrs
+        if name == "fwd":
+            fwd_a[(tag, li)] = a
         out = torch.empty(pp.out.numel(), dtype=torch.float32).pin_memory().numpy()
         host.append((a, b, pp, out, fl, name))
         tags.append(tag)
@@ -807,6 +803,22 @@ def e2e(args, sp, work, ws, rank, comm=None):
         if comm is not None and name == "bww":
             h2d += out.nbytes
             d2h += out.nbytes
+    # the batch call's operands: BWW (check = input) names the layer's ActNCHWc D -- the buffer its FWD pass
+    # uploads -- and the library packs ActCHWNn on the device (SPC_PASS_CHECKED_NCHWC); bytes it uploads: every
+    # buffer once per window of passes in flight (an activation the previous two passes uploaded is read in place)
+    batch_ops, h2d_shared, recent = [], 0, []
+    for (a, b, pp, out, fl, name), (tag, li, *_rest) in zip(host, work):
+        if name == "bww" and (tag, li) in fwd_a and sp.BwwCheck(pp.plan_obj.check) == sp.BwwCheck.input:
+            a = fwd_a[(tag, li)]
+        batch_ops.append((a, b))
+        seen = set().union(*recent) if recent else set()
+        mine = set()
+        for t in (a, b):
+            key = t.data.ctypes.data
+            mine.add(key)
+            if key not in seen or t.layout == sp.Layout.filter_kcrs_blk:
+                h2d_shared += t.data.nbytes
+        recent = (recent + [mine])[-2:]
     L = sp._lib.load()
     scratch = None
     if comm is not None:
@@ -863,7 +875,7 @@ def e2e(args, sp, work, ws, rank, comm=None):
         # bytes in and out, copies and kernels pipelined across passes (results bitwise those of the per-call
         # form: tests/test_gpu_parity.py::test_host_batch_equals_per_call)
         hb = sp.HostBatch()
-        for a, b, pp, out, fl, name in host:
+        for (a, b), (_a, _b, pp, out, fl, name) in zip(batch_ops, host):
             hb.add(a, b, pp.shape_obj, pp.plan_obj, sp.RunMode.sparse, out=out)
         hb.run()
         torch.cuda.synchronize()
@@ -876,14 +888,17 @@ def e2e(args, sp, work, ws, rank, comm=None):
         res.update({"value": round(flops / bsecs / 1e9, 1), "s_per_step": round(bsecs, 3),
                     "s_all_steps": [round(t, 3) for t in per], "statistic": "median step",
                     "h2d_bytes_per_step": int(h2d_shared),
-                    "h2d_note": "every distinct input buffer of the step is copied host->device inside the timed "
-                                "region; a layer's BWI and BWW name the same dY host buffer, which the batch call "
-                                "uploads once (per_call uploads it for each call)",
+                    "h2d_note": "every distinct input of the step (each layer's D, dY, filter and transposed filter) is "
+                                "copied host->device inside the timed region, once: a layer's BWI and BWW name the "
+                                "same dY host buffer, and its BWW names the ActNCHWc D its FWD uploads, packed "
+                                "into ActCHWNn on the device (SPC_PASS_CHECKED_NCHWC); per_call uploads the "
+                                "operands of every call, ActCHWNn D included",
                     "path": "spc_run_parallel_host_batch (include/spconv_b200.h): the step's passes in one call, "
                             "pinned host buffers, every input H2D and every output D2H inside the timed region, "
                             "pipelined across passes",
                     "per_call": per_call})
         del hb
+        sp.HostBatch.release()
     # pageable host memory (a std::vector caller): the same calls on the first
     # sparsity's passes (bounded host RAM), one step
     page = []

@@ -203,8 +203,18 @@ typedef struct {
     spc_tensor* dst;        /* data + capacity in, header out */
     spc_counters* counters; /* may be NULL */
     spc_status status;      /* out */
+    int flags;              /* SPC_PASS_* */
 } spc_host_pass;
+/* BWW only: the checked operand (plan.check: `a` for input, `b` for output_grad) is given in
+ * ActNCHWc instead of ActCHWNn and packed on the device by pack_act_chwnn's rule
+ * (P/src/tensor.cpp:94-108: ragged image lanes zero) -- the caller keeps one host layout of
+ * an activation, and a buffer an earlier pass of the batch already uploaded (a layer's FWD
+ * takes the same ActNCHWc input) is not uploaded again. */
+#define SPC_PASS_CHECKED_NCHWC 1
 spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n);
+/* The batch call keeps a per-thread device arena (8 passes in flight x the largest pass of the
+ * last batch) for its next call; this frees it. */
+void spc_host_batch_release(void);
 
 /* ---- ReLU semantics on device (P/src/sparsity.cpp:11-28), bit-exact ---- */
 spc_status spc_relu(const float* in, float* out, size_t n, void* stream);

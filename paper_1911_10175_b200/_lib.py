@@ -46,7 +46,10 @@ class spc_tensor(C.Structure):
 class spc_host_pass(C.Structure):
     _fields_ = [("a", C.POINTER(spc_tensor)), ("b", C.POINTER(spc_tensor)), ("shape", C.POINTER(spc_shape)),
                 ("plan", C.POINTER(spc_plan)), ("mode", C.c_int), ("dst", C.POINTER(spc_tensor)),
-                ("counters", C.POINTER(spc_counters)), ("status", C.c_int)]
+                ("counters", C.POINTER(spc_counters)), ("status", C.c_int), ("flags", C.c_int)]
+
+
+SPC_PASS_CHECKED_NCHWC = 1
 
 
 # name -> (restype, argtypes)
@@ -84,6 +87,7 @@ _SIGS = {
                                         C.POINTER(spc_plan), C.c_int, C.POINTER(spc_tensor),
                                         C.POINTER(spc_counters)]),
     "spc_run_parallel_host_batch": (C.c_int, [C.POINTER(spc_host_pass), C.c_int]),
+    "spc_host_batch_release": (None, []),
     "spc_relu": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_relu_grad_mask": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "spc_nchwc_to_chwnn": (C.c_int, [C.POINTER(spc_tensor), C.POINTER(spc_tensor), C.c_void_p]),

@@ -576,7 +576,10 @@ class HostBatch:
     and D2H copies are pipelined across passes.  ``add`` takes host (numpy)
     operands and an optional preallocated output; ``run`` executes every pass
     and returns one ConvResult per pass (counters included).  Buffers in
-    pinned memory are pipelined; pageable ones go through the per-call path."""
+    pinned memory are pipelined; pageable ones go through the per-call path.
+    A BWW pass may give its checked operand in ActNCHWc (the layout FWD takes):
+    the library packs ActCHWNn on the device (``SPC_PASS_CHECKED_NCHWC``), and a
+    buffer an earlier pass already uploaded is not uploaded again."""
 
     def __init__(self):
         self._keep = []
@@ -588,15 +591,25 @@ class HostBatch:
             raise SpconvError(_lib.SPC_ERR_ARG, "HostBatch takes host operands")
         desc, numel = output_desc(shape, pl)
         o = out if out is not None else np.empty(numel, np.float32)
+        flags = 0
+        if Component(pl.comp) == Component.bww:
+            checked = a if BwwCheck(pl.check) == BwwCheck.input else b
+            if checked.layout == Layout.act_nchwc:
+                flags = _lib.SPC_PASS_CHECKED_NCHWC
         item = dict(ca=a.to_c(), cb=b.to_c(), cs=shape.to_c(), cp=pl.to_c(), mode=int(mode),
                     cd=spc_tensor(0, 0, 0, 0, 0, 0, 0, 0, 0, o.ctypes.data, o.size), cnt=spc_counters(),
-                    out=o, desc=desc)
+                    out=o, desc=desc, flags=flags)
         self._keep.append((a, b))
         self._items.append(item)
         return len(self._items) - 1
 
     def __len__(self):
         return len(self._items)
+
+    @staticmethod
+    def release():
+        """Free the calling thread's device arena (kept between runs otherwise)."""
+        _lib.load().spc_host_batch_release()
 
     def run(self):
         L = _lib.load()
@@ -613,6 +626,7 @@ class HostBatch:
             arr[i].dst = C.pointer(it["cd"])
             arr[i].counters = C.pointer(it["cnt"])
             arr[i].status = 0
+            arr[i].flags = it["flags"]
         _check(L.spc_run_parallel_host_batch(arr, n))
         res = []
         for it in self._items:

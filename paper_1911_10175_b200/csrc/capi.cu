@@ -1073,14 +1073,14 @@ spc_status spc_run_parallel_host(const spc_tensor* a, const spc_tensor* b, const
 // passes: pass i+1's H2D starts while pass i's kernels and D2H are still in
 // flight, so the two copy engines and the SMs stay busy for the whole list
 // instead of draining at every call (the per-call form exposes each call's
-// first H2D chunk and last kernel + D2H chunk).  Up to batch_slots() passes are
+// first H2D chunk and last kernel + D2H chunk).  Up to batch_slots() (8) passes are
 // in flight, each in its own slice of a per-thread device arena (no
 // allocation inside the pipeline); every copy runs on the copy-in / copy-out
 // streams of the per-call path, every kernel on its compute stream.
 namespace {
-constexpr int kBatchSlotsMax = 8;
+constexpr int kBatchSlotsMax = 16;
 static int batch_slots() {
-    static const int v = std::getenv("SPC_BATCH_SLOTS") ? std::atoi(std::getenv("SPC_BATCH_SLOTS")) : 3;
+    static const int v = std::getenv("SPC_BATCH_SLOTS") ? std::atoi(std::getenv("SPC_BATCH_SLOTS")) : 8;
     return v < 1 ? 1 : v > kBatchSlotsMax ? kBatchSlotsMax : v;
 }
 constexpr int kBatchChunks = 16;
@@ -1119,12 +1119,21 @@ thread_local BatchState g_bs;
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// SPC_PASS_CHECKED_NCHWC: the BWW checked operand arrives in ActNCHWc and is packed on the device
+bool checked_nchwc(const spc_host_pass& p) {
+    return p.plan->comp == SPC_BWW && (p.flags & SPC_PASS_CHECKED_NCHWC) != 0;
+}
+const spc_tensor* checked_of(const spc_host_pass& p) { return p.plan->check == SPC_CHECK_INPUT ? p.a : p.b; }
+// elements of the ActCHWNn form of an N x C x H x W activation
+size_t chwnn_numel(const spc_tensor& t, int V) { return (size_t)((t.n + V - 1) / V) * V * t.c * t.h * t.w; }
+
 // device bytes one pass needs in its slot
 size_t batch_need(const spc_host_pass& p, const spc_tensor& out, int nc) {
     const bool bww = p.plan->comp == SPC_BWW;
     size_t n = align256(p.a->numel * sizeof(float)) + align256(p.b->numel * sizeof(float)) +
                align256(out.numel * sizeof(float)) + align256(kBatchChunks * sizeof(spc_counters));
     if (bww && nc > 1) n += align256((size_t)nc * out.numel * sizeof(float));
+    if (checked_nchwc(p)) n += align256(chwnn_numel(*checked_of(p), p.plan->V) * sizeof(float));
     return n;
 }
 
@@ -1207,6 +1216,9 @@ spc_status batch_enqueue(BatchState& bs, BatchSlot& sl, int idx, const spc_host_
     spc_counters* dc = reinterpret_cast<spc_counters*>(m);
     m += align256(kBatchChunks * sizeof(spc_counters));
     float* dpart = reinterpret_cast<float*>(m);
+    if (bww && nc > 1) m += align256((size_t)nc * out.numel * sizeof(float));
+    float* dconv = reinterpret_cast<float*>(m);  // SPC_PASS_CHECKED_NCHWC: the device-packed ActCHWNn operand
+    const bool conv = checked_nchwc(p);
     sl.pass = idx;
     sl.nc = nc;
     sl.out = out;
@@ -1263,7 +1275,9 @@ spc_status batch_enqueue(BatchState& bs, BatchSlot& sl, int idx, const spc_host_
     if (!bchk) sl.up[0] = BatchSlot::Upload{hchk, chk->numel, dchk};
     if (oth && !both) sl.up[1] = BatchSlot::Upload{hoth, oth->numel, doth};
     sl.up_last_chunk = nc - 1;
-    const size_t chk_unit = chk->numel / units;
+    // conv: chk is ActNCHWc on the host and in `dchk`; the kernels read its ActCHWNn form in `dconv`
+    const size_t img_unit = conv ? chk->numel / shape->N : 0;                 // ActNCHWc, per image
+    const size_t chk_unit = conv ? (size_t)V * img_unit : chk->numel / units;  // ActCHWNn per block, or per image
     const size_t oth_unit = oth ? oth->numel / shape->N : 0;
     const size_t out_unit = bww ? 0 : out.numel / shape->N;
     for (int c = 0; c < nc && st == SPC_OK && ce == cudaSuccess; ++c) {
@@ -1272,18 +1286,31 @@ spc_status batch_enqueue(BatchState& bs, BatchSlot& sl, int idx, const spc_host_
         const int i1 = bww ? (u1 * V < shape->N ? u1 * V : shape->N) : u1;
         spc_shape shc = *shape;
         shc.N = i1 - i0;
-        if (!bchk)
-            ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
-                               (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        if (!bchk) {
+            if (conv)
+                ck(cudaMemcpyAsync(dchk + (size_t)i0 * img_unit, hchk + (size_t)i0 * img_unit,
+                                   (size_t)(i1 - i0) * img_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+            else
+                ck(cudaMemcpyAsync(dchk + (size_t)u0 * chk_unit, hchk + (size_t)u0 * chk_unit,
+                                   (size_t)(u1 - u0) * chk_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
+        }
         if (oth && !both)
             ck(cudaMemcpyAsync(doth + (size_t)i0 * oth_unit, hoth + (size_t)i0 * oth_unit,
                                (size_t)(i1 - i0) * oth_unit * sizeof(float), cudaMemcpyHostToDevice, sin));
         ck(cudaEventRecord(sl.in_done[c], sin));
         ck(cudaStreamWaitEvent(s0, sl.in_done[c], 0));
         spc_tensor tchk = *chk, toth, tb = *b, td = out;
-        tchk.data = dchk + (size_t)u0 * chk_unit;
+        tchk.data = (conv ? dconv : dchk) + (size_t)u0 * chk_unit;
         tchk.n = shc.N;
         tchk.numel = (size_t)(u1 - u0) * chk_unit;
+        if (conv) {  // pack this chunk's images into ActCHWNn on the compute stream (pack_act_chwnn's lane rule)
+            spc_tensor tsrc = *chk;
+            tsrc.data = dchk + (size_t)i0 * img_unit;
+            tsrc.n = shc.N;
+            tsrc.numel = (size_t)(i1 - i0) * img_unit;
+            st = spc_nchwc_to_chwnn(&tsrc, &tchk, s0);
+            if (st) break;
+        }
         if (oth) {
             toth = *oth;
             toth.data = doth + (size_t)i0 * oth_unit;
@@ -1354,6 +1381,61 @@ spc_status batch_finish(BatchSlot& sl, spc_host_pass* passes) {
 }
 }  // namespace
 
+// Frees the calling thread's batch arena (batch_slots() x the largest pass of the last batch; it is
+// otherwise kept for the next call).
+void spc_host_batch_release(void) {
+    if (g_bs.arena) {
+        cudaDeviceSynchronize();
+        cudaFree(g_bs.arena);
+    }
+    g_bs.arena = nullptr;
+    g_bs.slot_bytes = 0;
+}
+
+// SPC_PASS_CHECKED_NCHWC with pageable buffers: a plain synchronous path (upload, pack ActCHWNn on the
+// device, one device BWW, download) -- same values as the pipelined form up to the chunking of the sum.
+static spc_status run_bww_checked_nchwc_sync(spc_host_pass& p, const spc_tensor& out) {
+    const int V = p.plan->V;
+    const bool on_input = p.plan->check == SPC_CHECK_INPUT;
+    const spc_tensor* chk = on_input ? p.a : p.b;
+    const spc_tensor* oth = on_input ? p.b : p.a;
+    const size_t cn = chwnn_numel(*chk, V);
+    float *dn = nullptr, *dc = nullptr, *dq = nullptr, *dd = nullptr;
+    spc_counters* dcnt = nullptr;
+    cudaError_t e = cudaMalloc((void**)&dn, chk->numel * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dc, cn * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dq, oth->numel * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dd, out.numel * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&dcnt, sizeof(spc_counters));
+    spc_status st = SPC_OK;
+    if (e == cudaSuccess) e = cudaMemcpy(dn, chk->data, chk->numel * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dq, oth->data, oth->numel * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        spc_tensor tn = *chk, tc_ = *chk, tq = *oth, td = out;
+        tn.data = dn;
+        tc_.data = dc;
+        tc_.numel = cn;
+        tq.data = dq;
+        td.data = dd;
+        st = spc_nchwc_to_chwnn(&tn, &tc_, nullptr);
+        if (st == SPC_OK)
+            st = spc_sparse_bww(on_input ? &tc_ : &tq, on_input ? &tq : &tc_, p.shape, p.plan, p.mode, &td,
+                                p.counters ? dcnt : nullptr, nullptr);
+        if (st == SPC_OK) e = cudaMemcpy(out.data, dd, out.numel * sizeof(float), cudaMemcpyDeviceToHost);
+        if (st == SPC_OK && e == cudaSuccess && p.counters)
+            e = cudaMemcpy(p.counters, dcnt, sizeof(spc_counters), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(dn);
+    cudaFree(dc);
+    cudaFree(dq);
+    cudaFree(dd);
+    cudaFree(dcnt);
+    if (st) return st;
+    if (e != cudaSuccess) return cuda_fail(e, "host batch (checked ActNCHWc, pageable)");
+    *p.dst = out;
+    return SPC_OK;
+}
+
 spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
     NvtxRange r("spc_run_parallel_host_batch");
     if (n < 0 || (n > 0 && !passes)) return fail(SPC_ERR_ARG, "null pass list");
@@ -1370,10 +1452,29 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
         switch (p.plan->comp) {
         case SPC_FWD: st = validate_fwd(p.a, p.b, *p.shape, *p.plan); break;
         case SPC_BWI: st = validate_bwi(p.a, p.b, *p.shape, *p.plan); break;
-        case SPC_BWW: st = validate_bww(p.a, p.b, *p.shape, *p.plan); break;
+        case SPC_BWW:
+            if (p.flags & SPC_PASS_CHECKED_NCHWC) {
+                // the checked operand in ActNCHWc: validate the pass as if it were its ActCHWNn form
+                const spc_tensor* chk = checked_of(p);
+                if (chk->layout != SPC_LAYOUT_ACT_NCHWC || !valid_V(p.plan->V) ||
+                    chk->numel != (size_t)chk->n * chk->c * chk->h * chk->w) {
+                    st = fail(SPC_ERR_LAYOUT, "bww: SPC_PASS_CHECKED_NCHWC wants the checked tensor in ActNCHWc");
+                    break;
+                }
+                spc_tensor as_chwnn = *chk;
+                as_chwnn.layout = SPC_LAYOUT_ACT_CHWNN;
+                as_chwnn.numel = chwnn_numel(*chk, p.plan->V);
+                st = p.plan->check == SPC_CHECK_INPUT ? validate_bww(&as_chwnn, p.b, *p.shape, *p.plan)
+                                                      : validate_bww(p.a, &as_chwnn, *p.shape, *p.plan);
+            } else {
+                st = validate_bww(p.a, p.b, *p.shape, *p.plan);
+            }
+            break;
         default: st = fail(SPC_ERR_PLAN, "run_parallel: bad component");
         }
         if (st) return p.status = st;
+        if ((p.flags & ~SPC_PASS_CHECKED_NCHWC) || ((p.flags & SPC_PASS_CHECKED_NCHWC) && p.plan->comp != SPC_BWW))
+            return p.status = fail(SPC_ERR_ARG, "bad pass flags");
         if (p.mode != SPC_SPARSE && p.mode != SPC_DENSE) return p.status = fail(SPC_ERR_ARG, "bad run mode");
         outs[i] = *p.dst;
         if ((st = prepare_dst(*p.shape, *p.plan, &outs[i]))) return p.status = st;
@@ -1390,6 +1491,31 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
     if ((st = host_streams(hs))) return st;
     BatchState* bs = nullptr;
     if (slot_bytes && (st = batch_state(bs, slot_bytes))) return st;
+    // Keep the stream-ordered pool's memory across the call: batch_finish synchronises on events, and at
+    // every synchronisation point the pool would otherwise return what exceeds its 1 GiB release threshold
+    // (check_device) -- the BWW workspaces (planes, split partials: up to ~0.7 GB per pass) then come back
+    // through fresh driver allocations that stall the enqueueing thread (measured: steps of 0.56-0.76 s among
+    // 0.26 s ones).  The threshold is restored when the call returns.
+    cudaMemPool_t pool = nullptr;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        } else {
+            pool = nullptr;
+        }
+    }
+    struct PoolRestore {
+        cudaMemPool_t pool;
+        ~PoolRestore() {
+            if (pool) {
+                unsigned long long thr = 1ull << 30;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
+    } pool_restore{pool};
     auto forget_uploads = [&]() {  // device copies of host buffers are trusted only inside one call
         for (int k = 0; k < kBatchSlotsMax && bs; ++k) bs->slot[k].up[0] = bs->slot[k].up[1] = BatchSlot::Upload{};
     };
@@ -1408,7 +1534,8 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
         if (!direct[i]) {
             drain();
             if (first) break;
-            p.status = spc_run_parallel_host(p.a, p.b, p.shape, p.plan, p.mode, p.dst, p.counters);
+            p.status = checked_nchwc(p) ? run_bww_checked_nchwc_sync(p, outs[i])
+                                        : spc_run_parallel_host(p.a, p.b, p.shape, p.plan, p.mode, p.dst, p.counters);
             if (p.status) first = p.status;
             forget_uploads();  // its output may overlap an uploaded range
             continue;

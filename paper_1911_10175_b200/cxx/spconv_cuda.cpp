@@ -109,8 +109,12 @@ std::vector<conv_result> run_batch(const std::vector<pass_request>& passes) {
         cd[i].data = r.out.data.data();
         cd[i].numel = r.out.data.size();
         std::memset(&cnt[i], 0, sizeof(spc_counters));
+        // a BWW checked operand given in act_nchwc is packed into act_chwnn on the device
+        const blocked_tensor& chk = p.plan.check == bww_check::input ? *p.a : *p.b;
+        const int flags =
+            p.plan.comp == component::bww && chk.layout == tensor_layout::act_nchwc ? SPC_PASS_CHECKED_NCHWC : 0;
         hp[i] = spc_host_pass{&ca[i], &cb[i], &cs[i], &cp[i], p.mode == run_mode::sparse ? SPC_SPARSE : SPC_DENSE,
-                              &cd[i], &cnt[i], SPC_OK};
+                              &cd[i], &cnt[i], SPC_OK, flags};
     }
     check(spc_run_parallel_host_batch(hp.data(), (int)n));
     for (size_t i = 0; i < n; ++i) {

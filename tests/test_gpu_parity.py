@@ -850,6 +850,46 @@ def test_host_batch_at_size_with_shared_dy(sp):
         assert gr.counters == w.counters, i
 
 
+def test_host_batch_packs_the_bww_checked_operand_on_device(sp):
+    """SPC_PASS_CHECKED_NCHWC: a batch BWW whose checked operand is the ActNCHWc
+    buffer (shared with the layer's FWD pass, so it is uploaded once) equals the
+    per-call BWW on the host-packed ActCHWNn operand, bitwise, for both check
+    sides, ragged batches (N % 16 != 0), pinned and pageable buffers."""
+    import torch
+    V = 16
+    pin = lambda t: sp.BlockedTensor(**{**t.header(), "data": torch.from_numpy(t.data).pin_memory().numpy()})
+    for (n, C, K, H, W), pinned in [((40, 32, 128, 14, 14), True), ((19, 64, 64, 9, 10), True),
+                                     ((33, 128, 128, 7, 7), False)]:
+        sh = sp.ConvShape.make(n, C, K, H, W, 3, 3, 1, 1)
+        D = O.gen_sparse(n, C, H, W, 0.6, n)
+        G = O.gen_sparse(K, C, 3, 3, 0.0, n + 1)
+        dY = O.gen_sparse(n, K, H, W, 0.5, n + 2)
+        nD, nY, bG = sp.pack_act_nchwc(D, V), sp.pack_act_nchwc(dY, V), sp.pack_filter(G, V)
+        if pinned:
+            nD, nY, bG = pin(nD), pin(nY), pin(bG)
+        pf = sp.plan(sh, sp.Component.fwd, V)
+        pi = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck.input)
+        po = sp.plan(sh, sp.Component.bww, V, 30, sp.BwwCheck.output_grad)
+        want = [sp.run_parallel(nD, bG, sh, pf, sp.RunMode.sparse),
+                sp.run_parallel(sp.pack_act_chwnn(D, V), nY, sh, pi, sp.RunMode.sparse),
+                sp.run_parallel(nD, sp.pack_act_chwnn(dY, V), sh, po, sp.RunMode.sparse)]
+        hb = sp.HostBatch()
+        hb.add(nD, bG, sh, pf)      # FWD uploads D (ActNCHWc)
+        hb.add(nD, nY, sh, pi)      # BWW check=input: D again, in ActNCHWc -> packed on the device
+        hb.add(nD, nY, sh, po)      # BWW check=output_grad: dY in ActNCHWc -> packed on the device
+        for rep in range(2):
+            got = hb.run()
+            for i, (g, w) in enumerate(zip(got, want)):
+                assert np.array_equal(g.out.data, w.out.data), (sh, pinned, i)
+                assert g.counters == w.counters, (sh, pinned, i)
+    # the flag is BWW-only and wants ActNCHWc
+    with pytest.raises(sp.SpconvError):
+        bad = sp.HostBatch()
+        bad.add(sp.pack_act_chwnn(D, V), nY, sh, pi)
+        bad._items[0]["flags"] = 1
+        bad.run()
+
+
 def test_host_batch_validates_every_pass_before_device_work(sp):
     V = 16
     sh = sp.ConvShape.make(2, 16, 16, 5, 5, 3, 3, 1, 1)
