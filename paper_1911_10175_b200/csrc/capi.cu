@@ -255,6 +255,13 @@ static void analytic_counters(const spc_shape& sh, const spc_plan& pl, int mode,
 __global__ void counters_init_kernel(spc_counters* c, spc_counters v) { *c = v; }
 
 // ---------------------------------------------------------------- device
+// bytes of stream-ordered workspace kept cached between calls (SPC_POOL_KEEP_GB)
+static unsigned long long pool_keep_bytes() {
+    static const unsigned long long v =
+        (unsigned long long)(std::getenv("SPC_POOL_KEEP_GB") ? std::atoi(std::getenv("SPC_POOL_KEEP_GB")) : 1) << 30;
+    return v;
+}
+
 static spc_status check_device() {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);
@@ -276,7 +283,7 @@ static spc_status check_device() {
     // (e.g. PyTorch's) can use it
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        unsigned long long thr = 1ull << 30;
+        unsigned long long thr = pool_keep_bytes();
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     if (dev >= 0 && dev < 64) cached_ok[dev] = 1;
@@ -1511,7 +1518,7 @@ spc_status spc_run_parallel_host_batch(spc_host_pass* passes, int n) {
         cudaMemPool_t pool;
         ~PoolRestore() {
             if (pool) {
-                unsigned long long thr = 1ull << 30;
+                unsigned long long thr = pool_keep_bytes();
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
             }
         }
