@@ -27,6 +27,10 @@
 
 #include <cstdlib>
 
+#ifndef SPC_TMA_BWW_FFMA2_MIN
+#define SPC_TMA_BWW_FFMA2_MIN SPC_FFMA2_MIN  // FMAs per lane in a pixel block from which the packed form is used
+#endif
+
 namespace spc {
 
 using tc::mbar_arrive;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(NWC * 32, MINB)
                             for (int u = 0; u < 3; ++u) {
                                 const int ny = ry - v, nx = rx - u;
                                 if (ny < 0 || nx < 0 || ny >= TH || nx >= TW) continue;
-                                fma_lane(acc[cc][v * 3 + u], d, O[ny * TW + nx], ntap);
+                                fma_lane<KK, SPC_TMA_BWW_FFMA2_MIN>(acc[cc][v * 3 + u], d, O[ny * TW + nx], ntap);
                             }
                         }
                     }
