@@ -870,35 +870,55 @@ def e2e(args, sp, work, ws, rank, comm=None):
            "d2h_bytes_per_step": int(d2h), "s_per_step": per_call["s_per_step"],
            "path": "spc_run_parallel_host (include/spconv_b200.h), pinned host buffers, per-call H2D+D2H+sync"
                    + ("; BWW dG allreduced across ranks" if comm is not None else "")}
-    if comm is None:
-        # the same passes, same host buffers, as ONE spc_run_parallel_host_batch call per step: identical
-        # bytes in and out, copies and kernels pipelined across passes (results bitwise those of the per-call
-        # form: tests/test_gpu_parity.py::test_host_batch_equals_per_call)
-        hb = sp.HostBatch()
-        for (a, b), (_a, _b, pp, out, fl, name) in zip(batch_ops, host):
-            hb.add(a, b, pp.shape_obj, pp.plan_obj, sp.RunMode.sparse, out=out)
+    # the same passes, same host buffers, as ONE spc_run_parallel_host_batch call per step: copies and kernels
+    # pipelined across passes (results bitwise those of the per-call form:
+    # tests/test_gpu_parity.py::test_host_batch_equals_per_call); under N > 1 each rank runs its shard's batch, then
+    # every BWW's partial dG is summed across ranks (H2D, allreduce, D2H), as in the per-call form
+    hb = sp.HostBatch()
+    for (a, b), (_a, _b, pp, out, fl, name) in zip(batch_ops, host):
+        hb.add(a, b, pp.shape_obj, pp.plan_obj, sp.RunMode.sparse, out=out)
+
+    def batch_step():
         hb.run()
-        torch.cuda.synchronize()
-        per = []
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
-            hb.run()
-            per.append(time.perf_counter() - t0)
-        bsecs = sorted(per)[len(per) // 2]
-        res.update({"value": round(flops / bsecs / 1e9, 1), "s_per_step": round(bsecs, 3),
-                    "s_all_steps": [round(t, 3) for t in per], "statistic": "median step",
-                    "h2d_bytes_per_step": int(h2d_shared),
-                    "h2d_note": "every distinct input of the step (each layer's D, dY, filter and transposed filter) is "
-                                "copied host->device inside the timed region, once: a layer's BWI and BWW name the "
-                                "same dY host buffer, and its BWW names the ActNCHWc D its FWD uploads, packed "
-                                "into ActCHWNn on the device (SPC_PASS_CHECKED_NCHWC); per_call uploads the "
-                                "operands of every call, ActCHWNn D included",
-                    "path": "spc_run_parallel_host_batch (include/spconv_b200.h): the step's passes in one call, "
-                            "pinned host buffers, every input H2D and every output D2H inside the timed region, "
-                            "pipelined across passes",
-                    "per_call": per_call})
-        del hb
-        sp.HostBatch.release()
+        if comm is not None:
+            for a, b, pp, out, fl, name in host:
+                if name == "bww":
+                    d = scratch[:out.size]
+                    d.copy_(torch.from_numpy(out), non_blocking=True)
+                    comm.allreduce(d, torch.cuda.current_stream().cuda_stream)
+                    torch.from_numpy(out).copy_(d)
+
+    batch_step()
+    torch.cuda.synchronize()
+    if comm is not None:
+        import torch.distributed as dist
+        dist.barrier()
+    per = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        batch_step()
+        per.append(time.perf_counter() - t0)
+    bsecs = sorted(per)[len(per) // 2]
+    if comm is not None:
+        t = torch.tensor([bsecs], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        bsecs = float(t.item())
+    bww_out = sum(h[3].nbytes for h in host if h[5] == "bww") if comm is not None else 0
+    res.update({"value": round(flops / bsecs / 1e9, 1), "s_per_step": round(bsecs, 3),
+                "s_all_steps": [round(t, 3) for t in per], "statistic": "median step",
+                "h2d_bytes_per_step": int(h2d_shared + bww_out),
+                "h2d_note": "every distinct input of the step (each layer's D, dY, filter and transposed filter) is "
+                            "copied host->device inside the timed region, once: a layer's BWI and BWW name the "
+                            "same dY host buffer, and its BWW names the ActNCHWc D its FWD uploads, packed "
+                            "into ActCHWNn on the device (SPC_PASS_CHECKED_NCHWC); per_call uploads the "
+                            "operands of every call, ActCHWNn D included",
+                "path": "spc_run_parallel_host_batch (include/spconv_b200.h): the step's passes in one call, "
+                        "pinned host buffers, every input H2D and every output D2H inside the timed region, "
+                        "pipelined across passes"
+                        + ("; BWW dG allreduced across ranks after the batch" if comm is not None else ""),
+                "per_call": per_call})
+    del hb
+    sp.HostBatch.release()
     # pageable host memory (a std::vector caller): the same calls on the first
     # sparsity's passes (bounded host RAM), one step
     page = []
