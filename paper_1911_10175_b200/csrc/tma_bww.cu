@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(NWC * 32, MINB)
     tma_bww_kernel(const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapY, DevShape sh,
                    float* __restrict__ partial, int splits, unsigned long long* __restrict__ exec_ctr,
                    const int* __restrict__ sel, int want) {
+    static_assert(NWC <= 15, "one named barrier (ids 1..15) per warp");
     using G = TGeom<KK, CB, NWC, TH, TW, NSTAGE>;
     if (sel != nullptr && __ldg(sel) != want) return;
     constexpr int TAPS = G::TAPS, CRH = G::CRH, CRW = G::CRW, CRWP = G::CRWP, PLANE = G::PLANE;

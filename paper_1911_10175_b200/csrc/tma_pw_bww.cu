@@ -71,6 +71,7 @@ __global__ void __launch_bounds__((BK / 8) * (BC / 8), 2)
     if (__ldg(finite) == 0) return;  // dY holds Inf / NaN: pw_bww.cu's EXACT kernel runs instead
     constexpr int NT = (BK / 8) * (BC / 8);
     constexpr int NWARP = NT / 32;
+    static_assert(NWARP <= 15, "one named barrier (ids 1..15) per warp");
     constexpr int ABYTES = TP_RT * BK * 4, BBYTES = BC * TP_RT * 4, STAGE = ABYTES + BBYTES;
     extern __shared__ __align__(1024) uint8_t smem[];  // no static shared memory in this kernel: offset 0
     const uint32_t sbase = smem_u32(smem);
